@@ -1,0 +1,143 @@
+"""Generate the committed golden fixtures from the UNMODIFIED reference.
+
+Run here (where /root/reference exists) after `make -C oracle`:
+
+    python tests/golden/make_golden.py
+
+Every vector is produced by oracle/_ref/synq_golden, which links the
+reference's own sources (proj/src/*.cpp) and calls its public C++ API
+(random.hpp, adjacency.hpp, engine.hpp, benchmarks.hpp).  The fixtures pin
+both the C restatement (tests/test_oracle.py) and the CUDA path
+(tests/test_gpu_parity.py) to the reference without needing /root/reference
+at test time.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+import oracle as O  # noqa: E402
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def rng_vectors():
+    out = {}
+    for seed in (1, 42, 2**63 + 5, 0):
+        out[f"xs_{seed}"] = np.frombuffer(O.golden("rng", seed, 64), np.uint32)
+    out["uniform_7"] = np.frombuffer(O.golden("uniform", 7, 32), np.float64)
+    pairs = [(1, 0), (1, 1), (1, 2**32), (1, 2**32 + 141420), (123, 9999), (2**64 - 1, 3)]
+    out["derive_pairs"] = np.array(pairs, np.uint64)
+    out["derive_vals"] = np.array([int(O.golden("derive", m, i)) for m, i in pairs], np.uint64)
+    cases = [(99, 500, 0.12, 200), (1, 3200, 0.02, 200), (5, 56568, 0.1, 40), (3, 100, 0.0, 4),
+             (3, 100, 1.0, 4), (8, 0, 0.5, 4)]
+    for k, (s, m, p, n) in enumerate(cases):
+        out[f"binom_{k}"] = np.frombuffer(O.golden("binomial", s, m, p, n), np.uint32)
+    out["binom_cases"] = np.array([(s, m, p, n) for s, m, p, n in cases], np.float64)
+    scases = [(50, 0, 5000, 2024), (6, 10, 30, 9), (1000, 100, 60000, 5), (10, 20, 30, 11),
+              (1, 7, 8, 3), (0, 5, 10, 3), (3000, 0, 3200, 77)]
+    for k, (n, a, b, s) in enumerate(scases):
+        out[f"sorted_{k}"] = np.frombuffer(O.golden("sorted", n, a, b, s), np.uint32)
+    out["sorted_cases"] = np.array(scases, np.uint64)
+    raw = O.golden("fig2")
+    out["fig2_trace"] = np.frombuffer(raw[: 8 * 5 * 8], np.float64).reshape(8, 5)
+    out["fig2_out"] = np.frombuffer(raw[8 * 5 * 8:], np.uint32)
+    np.savez_compressed(os.path.join(HERE, "rng_construct.npz"), **out)
+
+
+def plan_vectors():
+    out = {}
+    import tempfile
+    for tag, model, n, seed in (("pp42", "pingpong", 0, 42), ("v400", "vogels", 400, 1),
+                                ("b1000", "brunel", 1000, 3)):
+        with tempfile.TemporaryDirectory() as td:
+            p = os.path.join(td, "plan.bin")
+            O.golden("plan", model, n, seed, p)
+            raw = open(p, "rb").read()
+        njobs, deg_max, pitch, neurons = np.frombuffer(raw[:16], np.uint32)
+        total = np.frombuffer(raw[16:24], np.uint64)[0]
+        rec = np.dtype([("n", "<u4"), ("a", "<u4"), ("b", "<u4"), ("o", "<u8")])
+        jobs = np.frombuffer(raw[24: 24 + 20 * njobs], rec)
+        deg = np.frombuffer(raw[24 + 20 * njobs:], np.uint32)
+        out[f"{tag}_hdr"] = np.array([njobs, deg_max, pitch, neurons, total], np.uint64)
+        out[f"{tag}_jobs"] = np.stack([jobs["n"], jobs["a"], jobs["b"], jobs["o"]], 1).astype(np.uint64)
+        out[f"{tag}_deg"] = deg
+    np.savez_compressed(os.path.join(HERE, "plans.npz"), **out)
+
+
+ADJ = [("vogels", 400, 1, True), ("pingpong", 0, 42, True), ("vogels", 4000, 1, False),
+       ("brunel", 2000, 7, False), ("brunel", 20000, 1, False)]
+
+
+def adj_vectors():
+    out, meta = {}, {}
+    for model, n, seed, full in ADJ:
+        nn, pitch, deg_max, cells = O.reference_adjacency(model, n, seed)
+        tag = f"{model.replace('+', 'p')}_{n}_s{seed}"
+        deg = (cells != 0xFFFFFFFF).sum(1).astype(np.uint32)
+        out[f"{tag}_deg"] = deg
+        if full:
+            out[f"{tag}_cells"] = cells
+        meta[tag] = {"model": model, "neurons": n, "seed": seed, "pitch": pitch,
+                     "deg_max": deg_max, "rows": nn, "edges": int(deg.sum()),
+                     "sha256": sha(cells)}
+    np.savez_compressed(os.path.join(HERE, "adjacency.npz"), **out)
+    return meta
+
+
+RUNS = [
+    # model, neurons, seed, steps, history, dt, delay
+    ("pingpong", 0, 42, 200, 0, 0, 0),
+    ("pingpong", 0, 5, 1000, 0, 0, 0),
+    ("vogels", 1000, 99, 3000, 0, 0, 0),
+    ("vogels", 4000, 1, 10000, 0, 0, 0),
+    ("brunel", 2000, 99, 3000, 0, 0, 0),
+    ("brunel", 20000, 1, 2000, 0, 0, 0),
+    ("brunel+", 400, 99, 1000, 0, 0, 0),
+    ("brunel+", 120, 2024, 400, 0, 0, 0),
+    ("brunel+", 80, 7, 200, 1, 0, 0),
+    ("brunel+", 90, 99, 333, 23, 0, 0),
+    ("vogels", 500, 3, 500, 0, 0.25, 3),
+]
+
+
+def run_vectors():
+    out, meta = {}, {}
+    for model, n, seed, steps, hist, dt, delay in RUNS:
+        r = O.reference_run(model, n, seed, steps, hist, dt, delay)
+        tag = f"{model.replace('+', 'p')}_{n}_s{seed}_t{steps}_h{hist}_d{delay}"
+        out[f"{tag}_counts"] = r.counts
+        out[f"{tag}_ids"] = r.ids
+        for i, f in enumerate(r.fields):
+            out[f"{tag}_f{i}"] = f
+        if r.syn is not None:
+            for i, f in enumerate(r.syn):
+                out[f"{tag}_syn{i}"] = f
+            out[f"{tag}_ages"] = r.ages
+        meta[tag] = {"model": model, "neurons": n, "seed": seed, "steps": steps,
+                     "history": hist, "dt": dt, "delay": delay, "counters": r.counters}
+    np.savez_compressed(os.path.join(HERE, "runs.npz"), **out)
+    return meta
+
+
+def main():
+    if not O.have_reference():
+        raise SystemExit("oracle/_ref not built (needs /root/reference): make -C oracle")
+    rng_vectors()
+    plan_vectors()
+    meta = {"adjacency": adj_vectors(), "runs": run_vectors()}
+    with open(os.path.join(HERE, "golden.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
