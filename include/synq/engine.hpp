@@ -1,0 +1,798 @@
+#pragma once
+// network<Model>: the reference's clock-driven simulator API
+// (proj/include/synq/engine.hpp:46-471) backed by B200 device state.
+//
+// Same constructor, init/step/run/flush, accessors and spike tap.  What runs
+// where:
+//   construction  host degree plan + device expansion (csrc/construct.cu)
+//   init          k_init_neurons / k_init_synapses
+//   step / run    population-delivery models (vogels, brunel, and any user
+//                 model specialising synq::population_delivery): ONE
+//                 cooperative persistent launch per batch of steps
+//                 (detail/persistent.cuh), bit-exact with the reference's
+//                 deterministic mode.
+//                 Every other model: a CUDA graph of per-step kernels
+//                 (detail/kernels.cuh); deterministic mode (or threads == 1)
+//                 selects ordered delivery, reproducing the reference's
+//                 sequential float accumulation order exactly.
+//   tap / spans   host mirrors synced lazily; the tap is replayed per batch
+//                 from a device frame log, in step order, before run()
+//                 returns.
+//
+// Compile translation units that include this header with nvcc
+// (-std=c++20 --expt-relaxed-constexpr -fmad=false -gencode
+// arch=compute_100a,code=sm_100a) and link libsynq.so.
+#if !defined(__CUDACC__)
+#error "synq/engine.hpp launches sm_100a kernels: compile this translation unit with nvcc"
+#endif
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <numeric>
+#include <span>
+#include <stdexcept>
+#include <type_traits>
+#include <vector>
+
+#include "synq/adjacency.hpp"
+#include "synq/detail/cuda_util.hpp"
+#include "synq/detail/device_graph.hpp"
+#include "synq/detail/kernels.cuh"
+#include "synq/detail/persistent.cuh"
+#include "synq/models/benchmarks.hpp"
+#include "synq/network_desc.hpp"
+#include "synq/random.hpp"
+#include "synq/soa.hpp"
+
+namespace synq {
+
+struct engine_options {
+    uint64_t seed = 1;
+    unsigned threads = 0;         // reference: CPU workers; here threads == 1 implies ordered delivery
+    bool deterministic = false;   // ordered (reference-exact) delivery on the generic path
+    uint32_t history_frames = 0;  // 0 = max(delay + 1, 50)
+    uint32_t pitch_align = 32;    // 32 u32 = 128-byte rows
+    bool debug_checks = false;    // per-batch frame checks (sorted / unique)
+    // ---- B200 extensions
+    uint32_t batch_steps = 0;  // steps per device batch (0 = auto)
+    int persistent = -1;       // -1 auto, 0 never, 1 require (population-delivery models)
+    uint32_t tiles = 0;        // persistent CTAs (0 = auto)
+};
+
+struct engine_counters {
+    uint64_t steps = 0;
+    uint64_t spikes = 0;
+    uint64_t deliveries = 0;
+    uint64_t synapse_updates = 0;
+    uint64_t expiry_batches = 0;
+    uint64_t frames_consumed = 0;
+};
+
+struct phase_seconds {
+    double construct = 0.0;
+    double init_neurons = 0.0;
+    double init_synapses = 0.0;
+    double simulate = 0.0;
+};
+
+struct engine_memory {
+    uint64_t neuron_fields = 0;
+    uint64_t neuron_rng = 0;
+    uint64_t spike_queues = 0;
+    uint64_t spike_bitmasks = 0;
+    uint64_t ages = 0;
+    uint64_t expirations = 0;
+    uint64_t adjacency = 0;
+    uint64_t synapse_fields = 0;
+    uint64_t total() const {
+        return neuron_fields + neuron_rng + spike_queues + spike_bitmasks + ages + expirations +
+               adjacency + synapse_fields;
+    }
+};
+
+inline constexpr uint32_t lazy_history_default = 50;
+
+namespace detail {
+template <class M>
+constexpr bool model_uses_rng() {
+    return dev::model_uses_rng<M>();
+}
+template <class M, class = void>
+struct population_ok : std::false_type {};
+template <class M>
+struct population_ok<M, std::enable_if_t<population_delivery<M>::available>> : std::true_type {};
+
+template <class FieldList, size_t I = 0>
+void alloc_fields(std::vector<dev_array<unsigned char>>& cols, dev::field_ptrs<FieldList>& ptrs,
+                  size_t n, cudaStream_t s) {
+    if constexpr (I < FieldList::count) {
+        using T = field_t<I, FieldList>;
+        cols[I].resize(std::max<size_t>(1, n) * sizeof(T));
+        cols[I].zero(s);
+        ptrs.p[I] = cols[I].get();
+        alloc_fields<FieldList, I + 1>(cols, ptrs, n, s);
+    }
+}
+template <class FieldList, size_t I = 0>
+uint64_t field_bytes() {
+    if constexpr (I < FieldList::count)
+        return sizeof(field_t<I, FieldList>) + field_bytes<FieldList, I + 1>();
+    else
+        return 0;
+}
+}  // namespace detail
+
+template <class Model>
+class network {
+public:
+    using model_type = Model;
+    using neuron_fields = typename Model::neuron_fields;
+    using synapse_fields = typename dev::synapse_fields_of<Model>::type;
+    static constexpr bool has_synapses = dev::synapse_fields_of<Model>::present;
+    static constexpr bool uses_rng = detail::model_uses_rng<Model>();
+    static constexpr bool population_model = detail::population_ok<Model>::value;
+
+    using neuron_store = soa_store<neuron_fields>;
+    using synapse_store = soa_store<synapse_fields>;
+    using tap_fn = std::function<void(int64_t, std::span<const uint32_t>)>;
+
+    network(network_desc desc, Model model, engine_options opt = {})
+        : desc_(std::move(desc)), model_(std::move(model)), opt_(opt) {
+        validate_or_throw(desc_);
+        n_ = desc_.neuron_count();
+        dt_ = static_cast<float>(desc_.dt);
+        delay_ = desc_.delay;
+        SYNQ_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        int dev = 0;
+        SYNQ_CUDA(cudaGetDevice(&dev));
+        SYNQ_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev));
+
+        auto t0 = clock::now();
+        graph_ = build_device_graph(desc_, opt_.seed, opt_.pitch_align, stream_);
+        timings_.construct = since(t0);
+
+        if constexpr (has_synapses) {
+            const uint32_t floor = delay_ + 1;
+            history_ = opt_.history_frames ? std::max(opt_.history_frames, floor)
+                                           : std::max(floor, lazy_history_default);
+        }
+        exact_ = opt_.deterministic || opt_.threads == 1;
+        allocate();
+        init();
+    }
+
+    ~network() {
+        if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+        if (stream_) {
+            cudaStreamSynchronize(stream_);
+            cudaStreamDestroy(stream_);
+        }
+    }
+    network(const network&) = delete;
+    network& operator=(const network&) = delete;
+
+    // (re)run the Init stage (engine.hpp:154-186)
+    void init() {
+        push_mirrors();
+        t_ = 0;
+        counters_ = {};
+        host_steps_done_ = 0;
+        step_measured_.clear();
+        step_spikes_host_.clear();
+        expiring_host_.clear();
+        const int64_t zero = 0;
+        SYNQ_CUDA(cudaMemcpyAsync(t_dev_.get(), &zero, sizeof zero, cudaMemcpyHostToDevice, stream_));
+        counters_dev_.zero(stream_);
+        qcount_.zero(stream_);
+        if (hist_) hist_.zero(stream_);
+        tile_ctr_.zero(stream_);
+        done_ctr_.zero(stream_);
+        tile_status_.zero(stream_);
+        if (finfo_) finfo_.zero(stream_);
+        log_cursor_.zero(stream_);
+        if (expiring_count_) expiring_count_.zero(stream_);
+        flags_.zero(stream_);
+        if (det_cnt_) {
+            det_cnt_.zero(stream_);
+            det_fill_.zero(stream_);
+        }
+        SYNQ_CUDA(cudaStreamSynchronize(stream_));
+
+        auto t0 = clock::now();
+        const int grid = grid_for(n_, 256);
+        dev::k_init_neurons<Model><<<grid, 256, 0, stream_>>>(model_, state(), opt_.seed);
+        SYNQ_CUDA(cudaGetLastError());
+        SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        timings_.init_neurons = since(t0);
+
+        if constexpr (has_synapses) {
+            t0 = clock::now();
+            ages_.zero(stream_);
+            for (auto& col : syn_cols_) col.zero(stream_);
+            if (graph_.edges)
+                dev::k_init_synapses<Model><<<grid_for(uint64_t(n_) * 32, 256), 256, 0, stream_>>>(model_, state());
+            SYNQ_CUDA(cudaGetLastError());
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            timings_.init_synapses = since(t0);
+        }
+        invalidate_mirrors();
+    }
+
+    void step() { run(1); }
+
+    void run(int64_t steps) {
+        if (steps <= 0) return;
+        push_mirrors();
+        auto t0 = clock::now();
+        while (steps > 0) {
+            const int64_t b = std::min<int64_t>(steps, batch_cap_);
+            run_batch(static_cast<uint32_t>(b));
+            steps -= b;
+        }
+        timings_.simulate += since(t0);
+        invalidate_mirrors();
+    }
+
+    // bring every synapse current (engine.hpp:226-234)
+    void flush() {
+        if constexpr (has_synapses) {
+            push_mirrors();
+            auto t0 = clock::now();
+            dev::k_catchup<Model><<<grid_for(uint64_t(n_) * 32, 256), 256, 0, stream_>>>(model_, state(), 1);
+            SYNQ_CUDA(cudaGetLastError());
+            pull_counters();
+            timings_.simulate += since(t0);
+            invalidate_mirrors();
+        }
+    }
+
+    int64_t now() const { return t_; }
+    float dt() const { return dt_; }
+    uint32_t delay() const { return delay_; }
+    uint32_t history_frames() const { return history_; }
+    uint32_t neuron_count() const { return n_; }
+    uint64_t edge_count() const { return graph_.edges; }
+    uint64_t synapse_capacity() const {
+        return has_synapses ? static_cast<uint64_t>(n_) * graph_.deg_max : 0;
+    }
+    const adjacency_list& graph() const {
+        if (!adj_mirror_) adj_mirror_ = std::make_unique<adjacency_list>(download_graph(graph_, stream_));
+        return *adj_mirror_;
+    }
+    const network_desc& desc() const { return desc_; }
+    const engine_counters& counters() const { return counters_; }
+    const phase_seconds& timings() const { return timings_; }
+    uint64_t seed() const { return opt_.seed; }
+    bool deterministic() const { return opt_.deterministic; }
+    unsigned worker_count() const { return persistent_ ? tiles_ : static_cast<unsigned>(sms_); }
+    bool persistent() const { return persistent_; }
+    bool exact() const { return exact_ || persistent_; }
+    uint64_t construction_fixups() const { return graph_.tie_fixups; }
+
+    void set_spike_tap(tap_fn fn) {
+        tap_ = std::move(fn);
+        ensure_log();
+    }
+
+    // measured-population spike counts per step, kept on the device and
+    // returned per batch (the reference's sim_runtime tap, sim_runtime.cpp:33-39)
+    void set_measure_range(uint32_t lo, uint32_t hi) {
+        meas_lo_ = lo;
+        meas_hi_ = hi;
+        reset_graph();
+    }
+    const std::vector<uint32_t>& step_measured() const { return step_measured_; }
+    const std::vector<uint32_t>& step_spike_counts() const { return step_spikes_host_; }
+
+    template <size_t I>
+    auto neuron_field() {
+        using T = field_t<I, neuron_fields>;
+        if (!nmirror_valid_[I]) {
+            SYNQ_CUDA(cudaMemcpyAsync(host_neurons_.template data<I>(), neuron_cols_[I].get(),
+                                      n_ * sizeof(T), cudaMemcpyDeviceToHost, stream_));
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            nmirror_valid_[I] = true;
+        }
+        ndirty_[I] = true;
+        return std::span<T>(host_neurons_.template data<I>(), n_);
+    }
+    template <size_t I>
+    auto synapse_field() {
+        static_assert(has_synapses);
+        using T = field_t<I, synapse_fields>;
+        const size_t cap = synapse_capacity();
+        if (!smirror_valid_[I]) {
+            SYNQ_CUDA(cudaMemcpyAsync(host_synapses_.template data<I>(), syn_cols_[I].get(),
+                                      cap * sizeof(T), cudaMemcpyDeviceToHost, stream_));
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            smirror_valid_[I] = true;
+        }
+        sdirty_[I] = true;
+        return std::span<T>(host_synapses_.template data<I>(), cap);
+    }
+    std::span<const uint32_t> ages() const {
+        if constexpr (has_synapses) {
+            ages_host_.resize(n_);
+            ages_.download(ages_host_.data(), n_, stream_);
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        }
+        return {ages_host_.data(), ages_host_.size()};
+    }
+    std::span<const uint32_t> expiring() const {
+        if constexpr (has_synapses) return {expiring_host_.data(), expiring_host_.size()};
+        return {};
+    }
+    Model& model() { return model_; }
+
+    engine_memory memory() const {
+        engine_memory m;
+        m.neuron_fields = detail::field_bytes<neuron_fields>() * n_;
+        m.neuron_rng = uses_rng ? uint64_t(n_) * sizeof(xorshift) : 0;
+        m.spike_bitmasks = hist_.bytes();
+        m.spike_queues = queue_.bytes() + qcount_.bytes() + finfo_.bytes();
+        m.ages = has_synapses ? uint64_t(n_) * 4 : 0;
+        m.expirations = has_synapses ? uint64_t(n_) * 4 : 0;
+        m.adjacency = graph_.bytes() + split_.bytes();
+        m.synapse_fields = detail::field_bytes<synapse_fields>() * synapse_capacity();
+        return m;
+    }
+
+private:
+    using clock = std::chrono::steady_clock;
+    static double since(clock::time_point t0) {
+        return std::chrono::duration<double>(clock::now() - t0).count();
+    }
+    int grid_for(uint64_t work, int block) const {
+        const uint64_t want = (work + block - 1) / block;
+        return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, 16ull * sms_)));
+    }
+
+    // ------------------------------------------------------------ setup
+    void allocate() {
+        neuron_cols_.resize(std::max<size_t>(1, neuron_fields::count));
+        detail::alloc_fields<neuron_fields>(neuron_cols_, nptrs_, n_, stream_);
+        host_neurons_.resize(n_);
+        if constexpr (uses_rng) rng_.resize(std::max<uint32_t>(1, n_));
+        if constexpr (has_synapses) {
+            const size_t cap = synapse_capacity();
+            syn_cols_.resize(std::max<size_t>(1, synapse_fields::count));
+            detail::alloc_fields<synapse_fields>(syn_cols_, sptrs_, cap, stream_);
+            host_synapses_.resize(cap);
+            ages_.resize(std::max<uint32_t>(1, n_));
+            expiring_.resize(std::max<uint32_t>(1, n_));
+            expiring_count_.resize(1);
+            hist_words_ = (history_ + 63) / 64;
+            if (hist_words_ > 4) throw std::invalid_argument("history_frames above 256 are not supported");
+            hist_.resize(std::max<size_t>(1, size_t(n_) * hist_words_));
+        }
+        counters_dev_.resize(dev::C_COUNT);
+        tile_ctr_.resize(2);
+        done_ctr_.resize(1);
+        t_dev_.resize(1);
+        t0_dev_.resize(1);
+        flags_.resize(4);
+        log_cursor_.resize(2);
+        ntiles_update_ = std::max<uint32_t>(1, (n_ + kUpdateBlock - 1) / kUpdateBlock);
+        tile_status_.resize(ntiles_update_);
+
+        if constexpr (population_model) {
+            if (opt_.persistent != 0) setup_persistent();
+            if (opt_.persistent == 1 && !persistent_)
+                throw std::invalid_argument("persistent engine requested but the network does not fit it");
+        }
+        Q_ = persistent_ ? 2 * delay_ : delay_;
+        queue_.resize(std::max<size_t>(1, size_t(Q_) * n_));
+        qcount_.resize(Q_);
+        if (!persistent_ && exact_) {
+            det_cnt_.resize(std::max<uint32_t>(1, n_));
+            det_off_.resize(std::max<uint32_t>(1, n_));
+            det_fill_.resize(std::max<uint32_t>(1, n_));
+            det_cap_ = std::max<uint64_t>(1, std::min<uint64_t>(graph_.edges, 1ull << 27));
+            det_ev_.resize(det_cap_);
+        }
+        batch_cap_ = opt_.batch_steps ? opt_.batch_steps : 1000;
+        step_spikes_dev_.resize(batch_cap_);
+        step_meas_dev_.resize(batch_cap_);
+        step_buf_.resize(2 * size_t(batch_cap_));
+    }
+
+    void setup_persistent() requires population_model {
+        const std::vector<uint32_t> indeg = in_degrees(graph_, stream_);
+        uint32_t C = opt_.tiles ? opt_.tiles
+                                : static_cast<uint32_t>(std::clamp<int64_t>(
+                                      (static_cast<int64_t>(n_) + 511) / 1024, 1, sms_));
+        C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), std::max<uint32_t>(1, n_)});
+        // cost per neuron: a fixed update share plus expected arrivals
+        std::vector<double> prefix(size_t(n_) + 1, 0.0);
+        for (uint32_t i = 0; i < n_; ++i) prefix[i + 1] = prefix[i] + 16.0 + 0.003 * indeg[i];
+        std::vector<uint32_t> lo(C + 1, n_);
+        lo[0] = 0;
+        for (uint32_t c = 1; c < C; ++c) {
+            const double target = prefix[n_] * c / C;
+            lo[c] = static_cast<uint32_t>(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
+            lo[c] = std::clamp(lo[c], lo[c - 1], n_);
+        }
+        lo[C] = n_;
+        std::vector<uint32_t> wlo(C);
+        uint32_t wcap = 1;
+        for (uint32_t c = 0; c < C; ++c) {
+            uint32_t a = lo[c], b = lo[c + 1];
+            while (a < b && indeg[a] == 0) ++a;
+            while (b > a && indeg[b - 1] == 0) --b;
+            wlo[c] = a < b ? a : lo[c + 1];
+            wcap = std::max(wcap, b - a);
+        }
+        uint32_t bound[dev::kMaxClasses] = {};
+        float delta[dev::kMaxClasses] = {};
+        const int K = population_delivery<Model>::classes(model_, n_, bound, delta);
+        const size_t spike_chunk = 1024;
+        const size_t smem = (size_t(K) * wcap + 3 * spike_chunk) * sizeof(uint32_t);
+        int max_smem = 0, dev = 0;
+        SYNQ_CUDA(cudaGetDevice(&dev));
+        SYNQ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        const size_t static_smem = (2 * (dev::kMaxTiles + 1) + 64) * sizeof(uint32_t);
+        if (K < 1 || K > dev::kMaxClasses || smem + static_smem > size_t(max_smem)) return;
+        SYNQ_CUDA(cudaFuncSetAttribute(dev::k_persistent<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        int per_sm = 0;
+        SYNQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_persistent<Model>,
+                                                                dev::kPersistThreads, smem));
+        if (per_sm < 1) return;
+
+        tiles_ = C;
+        tile_lo_host_ = lo;
+        tile_lo_.resize(C + 1);
+        tile_lo_.upload(lo.data(), C + 1, stream_);
+        win_lo_.resize(C);
+        win_lo_.upload(wlo.data(), C, stream_);
+        build_splits(graph_, lo, split_, stream_);
+        finfo_.resize(size_t(2) * delay_ * C);
+        K_ = K;
+        std::copy(bound, bound + dev::kMaxClasses, bound_);
+        std::copy(delta, delta + dev::kMaxClasses, delta_);
+        win_cap_ = wcap;
+        spike_chunk_ = spike_chunk;
+        smem_ = smem;
+        persistent_ = true;
+    }
+
+    void reset_graph() {
+        if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+    }
+
+    void ensure_log() {
+        if (log_ids_ || log_pairs_) return;
+        reset_graph();
+        // frames of one batch; the batch shrinks to keep the log bounded
+        const uint64_t cap = std::max<uint64_t>(1024, std::min<uint64_t>(uint64_t(batch_cap_) * n_, 1ull << 26));
+        if (persistent_)
+            log_pairs_.resize(cap);
+        else
+            log_ids_.resize(cap);
+        log_cap_ = cap;
+        log_host_.resize(cap);
+        if (uint64_t(batch_cap_) * n_ > cap) batch_cap_ = std::max<uint32_t>(1, static_cast<uint32_t>(cap / std::max<uint32_t>(1, n_)));
+    }
+
+    dev::engine_state<Model> state() {
+        dev::engine_state<Model> s{};
+        s.nf = nptrs_;
+        s.sf = sptrs_;
+        s.rng = rng_.get();
+        s.cells = graph_.cells.get();
+        s.degree = graph_.degree.get();
+        s.n = n_;
+        s.pitch = graph_.pitch;
+        s.deg_max = graph_.deg_max;
+        s.queue = queue_.get();
+        s.qcount = qcount_.get();
+        s.Q = Q_;
+        s.hist = hist_.get();
+        s.hist_words = hist_words_;
+        s.ages = ages_.get();
+        s.expiring = expiring_.get();
+        s.expiring_count = expiring_count_.get();
+        s.counters = counters_dev_.get();
+        s.tile_status = tile_status_.get();
+        s.tile_ctr = tile_ctr_.get();
+        s.done_ctr = done_ctr_.get();
+        s.t_dev = t_dev_.get();
+        s.t0_dev = t0_dev_.get();
+        s.step_spikes = step_spikes_dev_.get();
+        s.step_meas = step_meas_dev_.get();
+        s.meas_lo = meas_lo_;
+        s.meas_hi = meas_hi_;
+        s.step_cap = batch_cap_;
+        s.log = log_ids_.get();
+        s.log_cursor = log_cursor_.get();
+        s.log_cap = log_cap_;
+        s.flags = flags_.get();
+        s.dt = dt_;
+        s.delay = delay_;
+        s.history = history_;
+        s.track_bits = has_synapses;
+        s.det_cnt = det_cnt_.get();
+        s.det_off = det_off_.get();
+        s.det_fill = det_fill_.get();
+        s.det_ev = det_ev_.get();
+        s.det_cap = det_cap_;
+        return s;
+    }
+
+    dev::persist_state<Model> pstate() requires population_model {
+        dev::persist_state<Model> p{};
+        p.nf = nptrs_;
+        p.rng = rng_.get();
+        p.cells = graph_.cells.get();
+        p.split = split_.get();
+        p.tile_lo = tile_lo_.get();
+        p.win_lo = win_lo_.get();
+        p.pitch = graph_.pitch;
+        p.n = n_;
+        p.C = tiles_;
+        p.queue = queue_.get();
+        p.finfo = finfo_.get();
+        p.Q = Q_;
+        p.K = K_;
+        std::copy(bound_, bound_ + dev::kMaxClasses, p.bound);
+        std::copy(delta_, delta_ + dev::kMaxClasses, p.delta);
+        p.dt = dt_;
+        p.delay = delay_;
+        p.counters = counters_dev_.get();
+        p.step_spikes = step_spikes_dev_.get();
+        p.step_meas = step_meas_dev_.get();
+        p.meas_lo = meas_lo_;
+        p.meas_hi = meas_hi_;
+        p.log = log_pairs_.get();
+        p.log_cursor = log_cursor_.get();
+        p.log_cap = log_cap_;
+        p.flags = flags_.get();
+        p.win_cap = win_cap_;
+        p.spike_chunk = spike_chunk_;
+        return p;
+    }
+
+    // ------------------------------------------------------------ stepping
+    static constexpr int kUpdateBlock = 256;
+    static constexpr int kReceiveBlock = 256;
+    static constexpr uint32_t kGraphSteps = 16;
+
+    void enqueue_generic_step() {
+        auto st = state();
+        dev::k_update<Model, kUpdateBlock><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
+        if constexpr (has_synapses)
+            dev::k_catchup<Model><<<grid_for(uint64_t(n_) * 32, 256), 256, 0, stream_>>>(model_, st, 0);
+        const int rgrid = 8 * sms_;
+        if (exact_) {
+            dev::k_det_events<Model, kReceiveBlock, false><<<rgrid, kReceiveBlock, 0, stream_>>>(st);
+            dev::k_det_scan<Model, 1024><<<1, 1024, 0, stream_>>>(st);
+            dev::k_det_events<Model, kReceiveBlock, true><<<rgrid, kReceiveBlock, 0, stream_>>>(st);
+            dev::k_det_apply<Model, kReceiveBlock><<<grid_for(n_, kReceiveBlock), kReceiveBlock, 0, stream_>>>(model_, st);
+        } else {
+            dev::k_receive<Model, kReceiveBlock><<<rgrid, kReceiveBlock, 0, stream_>>>(model_, st);
+        }
+    }
+
+    void ensure_graph() {
+        if (graph_exec_) return;
+        cudaGraph_t g = nullptr;
+        SYNQ_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        for (uint32_t k = 0; k < kGraphSteps; ++k) enqueue_generic_step();
+        SYNQ_CUDA(cudaStreamEndCapture(stream_, &g));
+        SYNQ_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+        cudaGraphDestroy(g);
+    }
+
+    void run_batch(uint32_t b) {
+        step_spikes_dev_.zero(stream_);
+        step_meas_dev_.zero(stream_);
+        const unsigned long long zero2[2] = {0, 0};
+        if (log_ids_ || log_pairs_)
+            SYNQ_CUDA(cudaMemcpyAsync(log_cursor_.get(), zero2, sizeof zero2, cudaMemcpyHostToDevice, stream_));
+        if (persistent_) {
+            if constexpr (population_model) {
+                auto ps = pstate();
+                int64_t t0 = t_;
+                int32_t nsteps = static_cast<int32_t>(b);
+                Model m = model_;
+                void* args[] = {&m, &ps, &t0, &nsteps};
+                SYNQ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_persistent<Model>),
+                                                      dim3(tiles_), dim3(dev::kPersistThreads), args,
+                                                      smem_, stream_));
+            }
+        } else {
+            const int64_t t0 = t_;
+            SYNQ_CUDA(cudaMemcpyAsync(t0_dev_.get(), &t0, sizeof t0, cudaMemcpyHostToDevice, stream_));
+            uint32_t left = b;
+            if (left >= kGraphSteps) {
+                ensure_graph();
+                while (left >= kGraphSteps) {
+                    SYNQ_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+                    left -= kGraphSteps;
+                }
+            }
+            while (left--) enqueue_generic_step();
+        }
+        SYNQ_CUDA(cudaGetLastError());
+        step_spikes_dev_.download(step_buf_.data(), b, stream_);
+        step_meas_dev_.download(step_buf_.data() + b, b, stream_);
+        uint64_t logged = 0;
+        if (log_ids_ || log_pairs_) {
+            unsigned long long cur[2];
+            SYNQ_CUDA(cudaMemcpyAsync(cur, log_cursor_.get(), sizeof cur, cudaMemcpyDeviceToHost, stream_));
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            logged = persistent_ ? cur[0] : cur[(t_ + b) & 1];
+            logged = std::min<uint64_t>(logged, log_cap_);
+            if (persistent_)
+                log_pairs_.download(log_host_.data(), logged, stream_);
+            else
+                log_ids_.download(reinterpret_cast<uint32_t*>(log_host_.data()), logged, stream_);
+        }
+        pull_counters();  // synchronises
+        if (flags_host_[0]) throw device_error("spike log overflow (batch too large for the frame log)");
+        if (flags_host_[1]) throw device_error("ordered delivery scratch overflow");
+
+        // per-step bookkeeping, frames_consumed (engine.hpp:371-380)
+        for (uint32_t k = 0; k < b; ++k) {
+            step_spikes_host_.push_back(step_buf_[k]);
+            step_measured_.push_back(step_buf_[b + k]);
+            if (t_ + k - int64_t(delay_) + 1 >= 0) ++counters_.frames_consumed;
+        }
+        counters_.steps += b;
+        if (log_ids_ || log_pairs_) replay_taps(b, logged);
+        t_ += b;
+    }
+
+    void replay_taps(uint32_t b, uint64_t logged) {
+        std::vector<uint32_t> frame;
+        if (persistent_) {
+            unsigned long long* p = log_host_.data();
+            std::sort(p, p + logged);
+            uint64_t q = 0;
+            for (uint32_t k = 0; k < b; ++k) {
+                const int64_t t = t_ + k;
+                frame.clear();
+                while (q < logged && static_cast<int64_t>(p[q] >> 32) == t) frame.push_back(uint32_t(p[q++]));
+                emit(t, frame);
+            }
+        } else {
+            const uint32_t* ids = reinterpret_cast<const uint32_t*>(log_host_.data());
+            uint64_t off = 0;
+            for (uint32_t k = 0; k < b; ++k) {
+                const uint32_t cnt = step_buf_[k];
+                frame.assign(ids + off, ids + std::min<uint64_t>(off + cnt, logged));
+                off += cnt;
+                emit(t_ + k, frame);
+            }
+        }
+    }
+
+    void emit(int64_t t, const std::vector<uint32_t>& frame) {
+        if (opt_.debug_checks)
+            for (size_t i = 1; i < frame.size(); ++i)
+                if (frame[i - 1] >= frame[i]) throw std::logic_error("spike frame not sorted/unique");
+        if (tap_) tap_(t, std::span<const uint32_t>(frame.data(), frame.size()));
+    }
+
+    void pull_counters() {
+        unsigned long long c[dev::C_COUNT];
+        counters_dev_.download(c, dev::C_COUNT, stream_);
+        flags_.download(flags_host_, 4, stream_);
+        SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        counters_.spikes = c[dev::C_SPIKES];
+        counters_.deliveries = c[dev::C_DELIVERIES];
+        counters_.synapse_updates = c[dev::C_SYN_UPDATES];
+        counters_.expiry_batches = c[dev::C_EXPIRY];
+    }
+
+    // ------------------------------------------------------------ mirrors
+    void invalidate_mirrors() {
+        std::fill(std::begin(nmirror_valid_), std::end(nmirror_valid_), false);
+        std::fill(std::begin(smirror_valid_), std::end(smirror_valid_), false);
+    }
+    template <size_t I = 0>
+    void push_neuron_cols() {
+        if constexpr (I < neuron_fields::count) {
+            using T = field_t<I, neuron_fields>;
+            if (ndirty_[I])
+                SYNQ_CUDA(cudaMemcpyAsync(neuron_cols_[I].get(), host_neurons_.template data<I>(),
+                                          n_ * sizeof(T), cudaMemcpyHostToDevice, stream_));
+            ndirty_[I] = false;
+            push_neuron_cols<I + 1>();
+        }
+    }
+    template <size_t I = 0>
+    void push_syn_cols() {
+        if constexpr (I < synapse_fields::count) {
+            using T = field_t<I, synapse_fields>;
+            if (sdirty_[I])
+                SYNQ_CUDA(cudaMemcpyAsync(syn_cols_[I].get(), host_synapses_.template data<I>(),
+                                          synapse_capacity() * sizeof(T), cudaMemcpyHostToDevice, stream_));
+            sdirty_[I] = false;
+            push_syn_cols<I + 1>();
+        }
+    }
+    void push_mirrors() {
+        push_neuron_cols();
+        if constexpr (has_synapses) push_syn_cols();
+        SYNQ_CUDA(cudaStreamSynchronize(stream_));
+    }
+
+    // ------------------------------------------------------------ members
+    network_desc desc_;
+    Model model_;
+    engine_options opt_;
+    uint32_t n_ = 0;
+    float dt_ = 1.0f;
+    uint32_t delay_ = 1;
+    uint32_t history_ = 0;
+    bool exact_ = false;
+    int sms_ = 148;
+    cudaStream_t stream_ = nullptr;
+
+    device_graph graph_;
+    mutable std::unique_ptr<adjacency_list> adj_mirror_;
+
+    std::vector<dev_array<unsigned char>> neuron_cols_, syn_cols_;
+    dev::field_ptrs<neuron_fields> nptrs_{};
+    dev::field_ptrs<synapse_fields> sptrs_{};
+    dev_array<xorshift> rng_;
+    dev_array<uint32_t> ages_, expiring_, expiring_count_;
+    dev_array<uint64_t> hist_;
+    uint32_t hist_words_ = 1;
+    dev_array<uint32_t> queue_, qcount_;
+    uint32_t Q_ = 1;
+    dev_array<unsigned long long> counters_dev_, tile_status_, log_cursor_;
+    dev_array<uint32_t> tile_ctr_, done_ctr_, flags_;
+    uint32_t ntiles_update_ = 1;
+    dev_array<int64_t> t_dev_, t0_dev_;
+    dev_array<uint32_t> step_spikes_dev_, step_meas_dev_;
+    pinned_array<uint32_t> step_buf_;
+    dev_array<uint32_t> det_cnt_, det_off_, det_fill_;
+    dev_array<unsigned long long> det_ev_;
+    uint64_t det_cap_ = 0;
+    dev_array<uint32_t> log_ids_;
+    dev_array<unsigned long long> log_pairs_;
+    pinned_array<unsigned long long> log_host_;
+    uint64_t log_cap_ = 0;
+    uint32_t flags_host_[4] = {0, 0, 0, 0};
+    cudaGraphExec_t graph_exec_ = nullptr;
+    uint32_t batch_cap_ = 1000;
+
+    // persistent engine
+    bool persistent_ = false;
+    uint32_t tiles_ = 0;
+    std::vector<uint32_t> tile_lo_host_;
+    dev_array<uint32_t> tile_lo_, win_lo_, split_;
+    dev_array<unsigned long long> finfo_;
+    int K_ = 0;
+    uint32_t bound_[dev::kMaxClasses] = {};
+    float delta_[dev::kMaxClasses] = {};
+    uint32_t win_cap_ = 0, spike_chunk_ = 0;
+    size_t smem_ = 0;
+
+    // host-visible state
+    neuron_store host_neurons_;
+    synapse_store host_synapses_;
+    bool nmirror_valid_[16] = {}, ndirty_[16] = {};
+    bool smirror_valid_[16] = {}, sdirty_[16] = {};
+    mutable std::vector<uint32_t> ages_host_;
+    std::vector<uint32_t> expiring_host_;
+    uint32_t meas_lo_ = 0, meas_hi_ = 0;
+    std::vector<uint32_t> step_measured_, step_spikes_host_;
+    uint64_t host_steps_done_ = 0;
+
+    int64_t t_ = 0;
+    tap_fn tap_;
+    engine_counters counters_;
+    phase_seconds timings_;
+};
+
+}  // namespace synq

@@ -1,0 +1,395 @@
+// Network construction on the B200.
+//
+// Reference: proj/src/adjacency.cpp:29-109 (plan_jobs / expand_jobs /
+// build_adjacency) and proj/include/synq/adjacency.hpp:112-163
+// (sorted_random).
+//
+// * plan_jobs stays on the host: it is ONE sequential binomial stream
+//   (derive_seed(seed, 0)) whose draw positions are data dependent, and glibc
+//   log/log1p decide the degrees, so the host reproduces it bit for bit.
+// * expansion runs on the device, one thread per job.  Each thread replays
+//   its job's xorshift stream twice (pass 1: the exclusive-sum total, pass 2:
+//   the outputs) with the same left-to-right double summation as the
+//   reference, and writes directly into the job's final position inside the
+//   row.  A source's jobs target disjoint populations, so ordering the jobs of
+//   a row by range start yields the sorted row the reference gets from
+//   std::sort — no sort pass on the device.
+// * exactness guard: CUDA's double log and glibc's may differ by an ulp.  A
+//   rigorous bound on the resulting error of v = prefix/total*scale is
+//   computed per job; any output whose v+0.5 lies within that bound of an
+//   integer flags the job, and flagged jobs are recomputed on the host with
+//   glibc and patched in.  The table is therefore bit-identical to the
+//   reference's.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <numeric>
+#include <stdexcept>
+#include <vector>
+
+#include "synq/adjacency.hpp"
+#include "synq/detail/device_graph.hpp"
+#include "synq/random.hpp"
+
+namespace synq {
+
+// ------------------------------------------------------------ host mirror
+adjacency_list::adjacency_list(uint32_t neurons, uint32_t deg_max, uint32_t row_pitch)
+    : neurons_(neurons), deg_max_(deg_max), pitch_(row_pitch) {
+    cells_.assign(static_cast<size_t>(neurons) * row_pitch, sentinel);
+    degree_.assign(neurons, 0);
+}
+
+adjacency_list::adjacency_list(uint32_t neurons, uint32_t deg_max, uint32_t row_pitch,
+                               std::vector<uint32_t> cells, std::vector<uint32_t> degree)
+    : neurons_(neurons), deg_max_(deg_max), pitch_(row_pitch), cells_(std::move(cells)),
+      degree_(std::move(degree)) {
+    edges_ = 0;
+    for (uint32_t d : degree_) edges_ += d;
+}
+
+std::span<const uint32_t> adjacency_list::row(uint32_t id) const {
+    if (id >= neurons_) throw std::out_of_range("adjacency row id out of range");
+    return {cells_.data() + static_cast<size_t>(id) * pitch_, degree_[id]};
+}
+
+std::span<const uint32_t> adjacency_list::raw_row(uint32_t id) const {
+    if (id >= neurons_) throw std::out_of_range("adjacency row id out of range");
+    return {cells_.data() + static_cast<size_t>(id) * pitch_, pitch_};
+}
+
+// binary format of adjacency.cpp:122-163: u32 neurons, pitch, deg_max,
+// sentinel, then neurons*pitch u32 cells; degrees are recovered on load
+void adjacency_list::dump(std::ostream& out) const {
+    const uint32_t hdr[4] = {neurons_, pitch_, deg_max_, sentinel};
+    out.write(reinterpret_cast<const char*>(hdr), sizeof hdr);
+    out.write(reinterpret_cast<const char*>(cells_.data()),
+              static_cast<std::streamsize>(cells_.size() * sizeof(uint32_t)));
+}
+
+adjacency_list adjacency_list::load(std::istream& in) {
+    uint32_t hdr[4] = {0, 0, 0, 0};
+    in.read(reinterpret_cast<char*>(hdr), sizeof hdr);
+    if (!in || hdr[3] != sentinel) throw std::runtime_error("adjacency load: bad header");
+    adjacency_list adj(hdr[0], hdr[2], hdr[1]);
+    in.read(reinterpret_cast<char*>(adj.cells_.data()),
+            static_cast<std::streamsize>(adj.cells_.size() * sizeof(uint32_t)));
+    if (!in) throw std::runtime_error("adjacency load: truncated data");
+    adj.edges_ = 0;
+    for (uint32_t r = 0; r < adj.neurons_; ++r) {
+        const uint32_t* row = adj.cells_.data() + static_cast<size_t>(r) * adj.pitch_;
+        uint32_t d = 0;
+        while (d < adj.pitch_ && row[d] != sentinel) ++d;
+        adj.degree_[r] = d;
+        adj.edges_ += d;
+    }
+    return adj;
+}
+
+void adjacency_list::save_file(const std::string& path) const {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot open for writing: " + path);
+    dump(out);
+}
+
+adjacency_list adjacency_list::load_file(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open: " + path);
+    return load(in);
+}
+
+// ------------------------------------------------------------------ plan
+construction_plan plan_jobs(const network_desc& desc, uint64_t seed, uint32_t pitch_align) {
+    construction_plan plan;
+    const uint32_t n = desc.neuron_count();
+    plan.out_degree.assign(n, 0);
+    xorshift master(derive_seed(seed, 0));
+
+    // jobs are emitted source-major in connection order; count them first
+    std::vector<uint64_t> first(static_cast<size_t>(n) + 1, 0);
+    for (const auto& c : desc.connections) {
+        auto [sa, sb] = desc.id_range(c.src);
+        for (uint32_t s = sa; s < sb; ++s) ++first[s + 1];
+    }
+    std::partial_sum(first.begin(), first.end(), first.begin());
+    plan.jobs.resize(first[n]);
+    std::vector<uint32_t> filled(n, 0);
+
+    // the degree draws themselves consume the master stream connection by
+    // connection, source by source (adjacency.cpp:41-51)
+    for (const auto& c : desc.connections) {
+        auto [sa, sb] = desc.id_range(c.src);
+        auto [ta, tb] = desc.id_range(c.dst);
+        for (uint32_t s = sa; s < sb; ++s) {
+            const uint32_t k = binomial(tb - ta, c.p, master);
+            plan.out_degree[s] += k;
+            plan.jobs[first[s] + filled[s]++] = construction_job{k, ta, tb, 0};
+        }
+    }
+    for (uint32_t d : plan.out_degree) plan.deg_max = std::max(plan.deg_max, d);
+    if (pitch_align == 0) pitch_align = 1;
+    plan.row_pitch = (plan.deg_max + pitch_align - 1) / pitch_align * pitch_align;
+    for (uint32_t s = 0; s < n; ++s) {
+        uint64_t o = static_cast<uint64_t>(s) * plan.row_pitch;
+        for (uint64_t q = first[s]; q < first[s + 1]; ++q) {
+            plan.jobs[q].o = o;
+            o += plan.jobs[q].n;
+            plan.total_edges += plan.jobs[q].n;
+        }
+    }
+    return plan;
+}
+
+// ------------------------------------------------------------- expansion
+namespace {
+
+struct dev_job {
+    uint32_t n, a, b, pad;
+    uint64_t o;      // final (sorted) offset of the job's first output
+    uint64_t index;  // position in plan order: the stream is derive_seed(seed, index + 1)
+};
+
+// rigorous per-job bound on |v_device - v_host| for v = prefix/total*scale
+// when the two logs may differ by <= 2 ulp (see file comment)
+__host__ __device__ inline double tie_guard(uint32_t n, double scale) {
+    return 2.0 * scale * (6.0 * (n + 2.0) + 24.0) * 0x1p-52 + 1e-12;
+}
+
+__global__ void k_expand(const dev_job* __restrict__ jobs, uint64_t njobs, uint64_t seed,
+                         uint32_t* __restrict__ cells, uint64_t* __restrict__ flagged,
+                         unsigned long long* __restrict__ nflagged, uint64_t flag_cap) {
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < njobs;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const dev_job job = jobs[j];
+        if (job.n == 0) continue;
+        const uint64_t stream = derive_seed(seed, job.index + 1);
+        // pass 1: total = sum of the first n+1 exponentials, left to right
+        xorshift r(stream);
+        double total = 0.0;
+        for (uint32_t i = 0; i <= job.n; ++i) total += -log(r.uniform01());
+        if (total <= 0.0) total = 1.0;
+        const double scale = static_cast<double>(job.b - job.a - job.n);
+        const double guard = tie_guard(job.n, scale);
+        // pass 2: replay the stream, emit a + round_half_up(prefix/total*scale) + i
+        r = xorshift(stream);
+        double prefix = 0.0;
+        bool close = false;
+        uint32_t* out = cells + job.o;
+        for (uint32_t i = 0; i < job.n; ++i) {
+            prefix += -log(r.uniform01());
+            const double v = prefix / total * scale;
+            const double f = floor(v + 0.5);
+            const double d = (v + 0.5) - f;
+            close |= (d < guard) || (1.0 - d < guard);
+            out[i] = job.a + static_cast<uint32_t>(f) + i;
+        }
+        if (close) {
+            const unsigned long long slot = atomicAdd(nflagged, 1ull);
+            if (slot < flag_cap) flagged[slot] = j;
+        }
+    }
+}
+
+__global__ void k_in_degree(const uint32_t* __restrict__ cells, const uint32_t* __restrict__ degree,
+                            uint32_t neurons, uint32_t pitch, uint32_t* __restrict__ indeg) {
+    // one warp per row: rows are short relative to the grid, lanes stride the row
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t s = warp; s < neurons; s += nwarps) {
+        const uint32_t d = degree[s];
+        const uint32_t* row = cells + s * pitch;
+        for (uint32_t k = lane; k < d; k += 32) atomicAdd(&indeg[row[k]], 1u);
+    }
+}
+
+__global__ void k_splits(const uint32_t* __restrict__ cells, const uint32_t* __restrict__ degree,
+                         uint32_t neurons, uint32_t pitch, const uint32_t* __restrict__ tile_lo,
+                         uint32_t tiles, uint32_t* __restrict__ split) {
+    const uint64_t total = static_cast<uint64_t>(neurons) * (tiles + 1);
+    for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+         x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t s = x / (tiles + 1);
+        const uint32_t c = static_cast<uint32_t>(x % (tiles + 1));
+        const uint32_t d = degree[s];
+        uint32_t pos;
+        if (c == tiles) {
+            pos = d;
+        } else {
+            const uint32_t key = tile_lo[c];
+            const uint32_t* row = cells + s * pitch;
+            uint32_t lo = 0, hi = d;  // lower_bound
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (row[mid] < key)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            pos = lo;
+        }
+        split[x] = pos;
+    }
+}
+
+int grid_for(uint64_t work, int block) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (work + block - 1) / block;
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, 32ull * sms)));
+}
+
+}  // namespace
+
+device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons, uint64_t seed,
+                                 cudaStream_t stream) {
+    device_graph g;
+    g.neurons = neurons;
+    g.deg_max = plan.deg_max;
+    g.pitch = plan.row_pitch;
+    g.edges = plan.total_edges;
+    g.jobs = plan.jobs.size();
+    g.host_degree = plan.out_degree;
+    g.host_degree.resize(neurons, 0);
+
+    const size_t ncells = static_cast<size_t>(neurons) * g.pitch;
+    g.cells.resize(ncells);
+    g.cells.fill_bytes(0xff, stream);  // sentinel padding
+    g.degree.resize(neurons);
+    g.degree.upload(g.host_degree.data(), neurons, stream);
+
+    // final offsets: a row's non-empty jobs ordered by target-range start.
+    // A non-empty job's offset lies strictly inside its row, so o / pitch is
+    // its source; empty jobs write nothing and are dropped.
+    std::vector<dev_job> jobs;
+    jobs.reserve(plan.jobs.size());
+    for (size_t q = 0; q < plan.jobs.size(); ++q) {
+        const auto& pj = plan.jobs[q];
+        if (pj.n == 0) continue;
+        jobs.push_back(dev_job{pj.n, pj.a, pj.b, 0, pj.o, static_cast<uint64_t>(q)});
+    }
+    for (size_t q = 0; q < jobs.size();) {
+        const uint64_t row = jobs[q].o / g.pitch;
+        size_t e = q + 1;
+        while (e < jobs.size() && jobs[e].o / g.pitch == row) ++e;
+        std::stable_sort(jobs.begin() + q, jobs.begin() + e,
+                         [](const dev_job& x, const dev_job& y) { return x.a < y.a; });
+        uint64_t o = row * g.pitch;
+        for (size_t k = q; k < e; ++k) {
+            jobs[k].o = o;
+            o += jobs[k].n;
+        }
+        q = e;
+    }
+
+    dev_array<dev_job> djobs(std::max<size_t>(1, jobs.size()));
+    djobs.upload(jobs.data(), jobs.size(), stream);
+    const uint64_t flag_cap = 1u << 20;
+    dev_array<uint64_t> flagged(flag_cap);
+    dev_array<unsigned long long> nflag(1);
+    nflag.zero(stream);
+    if (!jobs.empty()) {
+        k_expand<<<grid_for(jobs.size(), 128), 128, 0, stream>>>(
+            djobs.get(), jobs.size(), seed, g.cells.get(), flagged.get(), nflag.get(), flag_cap);
+        SYNQ_CUDA(cudaGetLastError());
+    }
+    unsigned long long nf = 0;
+    nflag.download(&nf, 1, stream);
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+
+    // host fix-up of guard-flagged jobs: glibc log, the reference's exact path
+    std::vector<uint64_t> fl(std::min<unsigned long long>(nf, flag_cap));
+    flagged.download(fl.data(), fl.size(), stream);
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+    if (nf > flag_cap) {
+        // too many to list: recompute every job on the host (never expected)
+        fl.resize(jobs.size());
+        std::iota(fl.begin(), fl.end(), 0);
+    }
+    std::vector<uint32_t> buf;
+    for (uint64_t j : fl) {
+        const dev_job& job = jobs[j];
+        buf.resize(job.n);
+        xorshift r(derive_seed(seed, job.index + 1));
+        sorted_random(job.n, job.a, job.b, r, buf.data());
+        SYNQ_CUDA(cudaMemcpyAsync(g.cells.get() + job.o, buf.data(), job.n * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, stream));
+        SYNQ_CUDA(cudaStreamSynchronize(stream));
+    }
+    g.tie_fixups = fl.size();
+    return g;
+}
+
+device_graph build_device_graph(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
+                                cudaStream_t stream) {
+    return expand_device_graph(plan_jobs(desc, seed, pitch_align), desc.neuron_count(), seed,
+                               stream);
+}
+
+adjacency_list download_graph(const device_graph& g, cudaStream_t stream) {
+    std::vector<uint32_t> cells(static_cast<size_t>(g.neurons) * g.pitch);
+    g.cells.download(cells.data(), cells.size(), stream);
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+    return adjacency_list(g.neurons, g.deg_max, g.pitch, std::move(cells), g.host_degree);
+}
+
+device_graph upload_graph(const adjacency_list& adj, cudaStream_t stream) {
+    device_graph g;
+    g.neurons = adj.neuron_count();
+    g.deg_max = adj.deg_max();
+    g.pitch = adj.row_pitch();
+    g.edges = adj.edge_count();
+    g.host_degree.assign(adj.degrees(), adj.degrees() + g.neurons);
+    g.cells.resize(static_cast<size_t>(g.neurons) * g.pitch);
+    g.cells.upload(adj.cells(), g.cells.size(), stream);
+    g.degree.resize(g.neurons);
+    g.degree.upload(g.host_degree.data(), g.neurons, stream);
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+    return g;
+}
+
+std::vector<uint32_t> in_degrees(const device_graph& g, cudaStream_t stream) {
+    std::vector<uint32_t> out(g.neurons, 0);
+    if (!g.neurons) return out;
+    dev_array<uint32_t> indeg(g.neurons);
+    indeg.zero(stream);
+    if (g.edges) {
+        k_in_degree<<<grid_for(static_cast<uint64_t>(g.neurons) * 32, 256), 256, 0, stream>>>(
+            g.cells.get(), g.degree.get(), g.neurons, g.pitch, indeg.get());
+        SYNQ_CUDA(cudaGetLastError());
+    }
+    indeg.download(out.data(), g.neurons, stream);
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+    return out;
+}
+
+void build_splits(const device_graph& g, const std::vector<uint32_t>& tile_lo,
+                  dev_array<uint32_t>& split, cudaStream_t stream) {
+    const uint32_t tiles = static_cast<uint32_t>(tile_lo.size()) - 1;
+    dev_array<uint32_t> dlo(tile_lo.size());
+    dlo.upload(tile_lo.data(), tile_lo.size(), stream);
+    split.resize(std::max<size_t>(1, static_cast<size_t>(g.neurons) * (tiles + 1)));
+    const uint64_t work = static_cast<uint64_t>(g.neurons) * (tiles + 1);
+    if (work) {
+        k_splits<<<grid_for(work, 256), 256, 0, stream>>>(g.cells.get(), g.degree.get(), g.neurons,
+                                                           g.pitch, dlo.get(), tiles, split.get());
+        SYNQ_CUDA(cudaGetLastError());
+    }
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+}
+
+adjacency_list expand_jobs(const construction_plan& plan, uint32_t neurons, uint64_t seed,
+                           thread_pool*) {
+    device_graph g = expand_device_graph(plan, neurons, seed, nullptr);
+    return download_graph(g, nullptr);
+}
+
+adjacency_list build_adjacency(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
+                               thread_pool*) {
+    device_graph g = build_device_graph(desc, seed, pitch_align, nullptr);
+    return download_graph(g, nullptr);
+}
+
+}  // namespace synq
