@@ -1,0 +1,408 @@
+#!/usr/bin/env python3
+"""Headline benchmark: Brunel balanced network at ~1e9 synapses on B200.
+
+Metric (BASELINE.json): synaptic events/sec and wall time per 1 s of
+biological time.  One bench "step" = 1 s of biological time = 10,000
+simulation timesteps (dt = 0.1 ms) of synq::network<brunel_model>, run through
+the C ABI (libsynq.so.1).  Events = the engine's delivery counter, exactly the
+reference's `deliveries` (proj/include/synq/engine.hpp:408).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl synq|reference]
+
+* value: events/s over all ranks, device-timed (CUDA events recorded by the
+  library on its own stream around every run; max over ranks).
+* e2e: the same workload through the C ABI with spike recording on and the
+  raster copied into host buffers each step (device->host bytes counted).
+* roofline: the persistent step kernel (update + receive fused) — algorithmic
+  bytes per launch / kernel time vs the measured HBM copy bandwidth.
+* cpu_baseline: the UNMODIFIED reference (oracle/_ref/libsynq_ref.so, built
+  from /root/reference by oracle/Makefile) on a bounded sample of the same
+  network, on this host's cores.
+* --impl reference: the reference's own CPU simulator on all host threads.
+Inputs are larger than L2 (4.2 GB adjacency vs 126 MB L2), so no L2 flush.
+Under torchrun (N > 1) every rank runs its own 1e9-synapse replica (weak
+scaling); rank 0 prints the JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "synaptic events/sec & wall time per 1 s bio time (Brunel, 1/2/4/8 B200)"
+UNIT = "events/s"
+BIO_STEPS = 10000  # 1 s of biological time at dt = 0.1 ms
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="synq", choices=["synq", "reference"])
+    ap.add_argument("--synapses", type=float, default=1e9)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample-steps", type=int, default=1000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.out, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        self.out.flush()
+        self.out.seek(0)
+        rows = [r.split(",") for r in self.out.read().strip().splitlines() if r.strip()]
+        rows = [[x.strip() for x in r] for r in rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        busy = [r for r in rows if r[7].isdigit() and int(r[7]) > 0] or rows
+        mhz = [int(r[1]) for r in busy if r[1].isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in busy:
+            for k, name in enumerate(names):
+                if r[3 + k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None,
+                "sm_max_mhz": int(rows[0][2]) if rows[0][2].isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(busy)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic_per_step():
+    """dram bytes per simulation timestep of the persistent kernel, from the
+    committed ncu --set full capture summary (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            s = json.load(fh)
+        return float(s["dram_bytes_per_timestep"]), s.get("source")
+    except Exception:
+        return None, None
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_reference_sample(synapses: float, seed: int, sample_steps: int, threads: int,
+                         deterministic: bool, warm_steps: int = 200):
+    """Run the unmodified reference on a bounded sample; returns dict."""
+    import oracle
+
+    ref = oracle.RefLib()
+    L = ref.L
+    opts = L.synq_opts_new()
+    L.synq_opts_seed(opts, seed)
+    L.synq_opts_deterministic(opts, 1 if deterministic else 0)
+    L.synq_opts_threads(opts, threads)
+    sim = C.c_void_p()
+    st = L.synq_sim_new_for_synapses(b"brunel", int(synapses), opts, C.byref(sim))
+    if st != 0:
+        raise RuntimeError("reference: " + L.synq_last_error().decode())
+    L.synq_sim_run(sim, warm_steps)
+    t_sim0 = L.synq_sim_seconds(sim, 3)
+    d0 = _ref_deliveries(L, sim)
+    L.synq_sim_run(sim, sample_steps)
+    t_sim = L.synq_sim_seconds(sim, 3) - t_sim0
+    d = _ref_deliveries(L, sim) - d0
+    out = {"events": d, "sim_s": t_sim, "steps": sample_steps,
+           "construct_s": L.synq_sim_seconds(sim, 0), "neurons": int(L.synq_sim_neurons(sim)),
+           "synapses": int(L.synq_sim_synapses(sim))}
+    L.synq_sim_free(sim)
+    L.synq_opts_free(opts)
+    return out
+
+
+def _ref_deliveries(L, sim) -> int:
+    with tempfile.NamedTemporaryFile("r", suffix=".txt") as fh:
+        L.synq_sim_write_stats(sim, fh.name.encode())
+        for line in open(fh.name):
+            if line.startswith("deliveries="):
+                return int(line.split("=")[1])
+    raise RuntimeError("reference stats lack deliveries")
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    try:
+        import oracle
+
+        if not oracle.have_reference():
+            raise FileNotFoundError("oracle/_ref not built")
+    except Exception as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
+        return 0
+    threads = os.cpu_count() or 1
+    sample = max(100, int(os.environ.get("SYNQ_REF_SAMPLE_STEPS", 500)))
+    import oracle
+
+    ref = oracle.RefLib()
+    L = ref.L
+    opts = L.synq_opts_new()
+    L.synq_opts_seed(opts, args.seed)
+    L.synq_opts_threads(opts, threads)
+    sim = C.c_void_p()
+    if L.synq_sim_new_for_synapses(b"brunel", int(args.synapses), opts, C.byref(sim)) != 0:
+        print(json.dumps({"impl": "reference", "unavailable": L.synq_last_error().decode()}))
+        return 0
+    for _ in range(args.warmup):
+        L.synq_sim_run(sim, sample)
+    t0 = L.synq_sim_seconds(sim, 3)
+    d0 = _ref_deliveries(L, sim)
+    for _ in range(args.steps):
+        L.synq_sim_run(sim, sample)
+    secs = L.synq_sim_seconds(sim, 3) - t0
+    events = _ref_deliveries(L, sim) - d0
+    value = events / secs
+    bio_per_step = sample / BIO_STEPS
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1000.0,
+        "wall_s_per_bio_s": secs / (args.steps * bio_per_step),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference builder, seed %d)" % args.seed,
+        "config": {"workload": "brunel", "synapses": int(L.synq_sim_synapses(sim)),
+                   "neurons": int(L.synq_sim_neurons(sim)), "bio_ms_per_step": sample * 0.1,
+                   "mode": f"reference parallel, {threads} threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} x {sample} timesteps of Brunel 1e9 after "
+                                   f"{args.warmup} warm-up samples"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    L.synq_sim_free(sim)
+    L.synq_opts_free(opts)
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------ B200 arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    rank, world, local = dist_env()
+    torch = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    os.environ.setdefault("CUDA_DEVICE_ORDER", "PCI_BUS_ID")
+    import paper_1912_07423_b200 as synq
+
+    # the CUDA runtime picks the device from the current context: bind it
+    if world > 1:
+        torch.cuda.synchronize()
+
+    cpu_result = {}
+    cpu_thread = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        def _cpu():
+            try:
+                cpu_result.update(cpu_reference_sample(args.synapses, args.seed,
+                                                       args.cpu_sample_steps, 1, True))
+            except Exception as e:  # reported, never fatal
+                cpu_result["error"] = str(e)
+        cpu_thread = threading.Thread(target=_cpu, daemon=True)
+        cpu_thread.start()
+
+    t_setup = time.perf_counter()
+    opts = synq.Opts(seed=args.seed + rank, deterministic=True)
+    sim = synq.Sim("brunel", opts=opts, synapses=int(args.synapses))
+    setup_s = time.perf_counter() - t_setup
+    assert sim.persistent, "brunel must run on the persistent engine"
+
+    sim.run(args.warmup * BIO_STEPS)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    barrier()
+    dev0, ker0 = sim.device_time()
+    c0 = sim.counters()
+    l0 = sim.kernel_launches()
+    with ClockSampler(local) as clocks:
+        sim.run(args.steps * BIO_STEPS)
+    dev1, ker1 = sim.device_time()
+    c1 = sim.counters()
+    l1 = sim.kernel_launches()
+    barrier()
+    secs = dev1 - dev0
+    kern = ker1 - ker0
+    events = c1["deliveries"] - c0["deliveries"]
+    spikes = c1["spikes"] - c0["spikes"]
+
+    # e2e: spike recording on, raster copied to host buffers every step
+    import numpy as np
+
+    sim.set_record(True)
+    h0, d0b = sim.transfer_bytes()
+    ce0 = sim.counters()["deliveries"]
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        sim.run(BIO_STEPS)
+        steps_arr, ids_arr = sim.raster()
+        sim.set_record(True)  # clears the host raster, keeps recording
+    e2e_s = time.perf_counter() - t0
+    h1, d1b = sim.transfer_bytes()
+    e2e_events = sim.counters()["deliveries"] - ce0
+    raster_bytes_host = int(steps_arr.nbytes + ids_arr.nbytes)
+    sim.set_record(False)
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([secs, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        secs, e2e_s = float(t[0]), float(t[1])
+        e = torch.tensor([events, e2e_events, spikes], dtype=torch.float64, device="cuda")
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        events, e2e_events, spikes = float(e[0]), float(e[1]), float(e[2])
+
+    if rank != 0:
+        return 0
+
+    n = sim.neurons
+    n_exc = int(round(0.4 * n))
+    n_rec = n_exc + int(round(0.1 * n))
+    n_stim = n - n_rec
+    timesteps = args.steps * BIO_STEPS
+    launches = l1 - l0
+    # algorithmic bytes of the fused step kernel: 4 B per
+    # delivery (target id), 24 B per LIF neuron-step, 32 B per Poisson
+    # neuron-step (16 B stream read + write), 4 B per queued spike
+    alg = 4.0 * events + (24.0 * n_rec + 32.0 * n_stim) * timesteps * world + 4.0 * spikes
+    peak, peak_src = measured_peaks()
+    achieved = alg / kern / 1e9 / world if kern > 0 else 0.0
+    traffic_step, traffic_src = ncu_traffic_per_step()
+    per_launch_steps = timesteps / max(1, launches)
+    line = {
+        "metric": METRIC,
+        "value": events / secs,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1000.0,
+        "wall_s_per_bio_s": secs / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic: Brunel network built on device from seed %d (reference RNG streams)" % args.seed,
+        "config": {
+            "workload": "brunel_1e9" if args.synapses == 1e9 else "brunel",
+            "synapses": sim.synapses, "neurons": n, "bio_s_per_step": 1.0, "dt_ms": 0.1,
+            "delay_steps": sim.delay, "parallelism": f"dp{world} (replicas)" if world > 1 else "single",
+            "engine": "persistent target-tiled (exact)", "tiles": None,
+            "l2": "inputs larger than L2 (adjacency %.2f GB)" % (sim.synapses * 4 / 1e9),
+            "setup_s": round(setup_s, 2), "construction_fixups": sim.construction_fixups(),
+        },
+        "gpu_launches": launches,
+        "spikes_per_bio_s": spikes / args.steps / world,
+        "events_per_bio_s": events / args.steps / world,
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "synq::dev::k_persistent<brunel_model> (update+receive fused)",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": (traffic_step * per_launch_steps) if traffic_step else None,
+            "traffic_source": traffic_src,
+            "alg_bytes_per_launch": alg / world / max(1, launches),
+            "receive_only_GBps": 4.0 * events / world / kern / 1e9 if kern > 0 else 0.0,
+            "kernel_s": kern,
+            "peak_source": peak_src,
+        },
+        "e2e": {
+            "value": e2e_events / e2e_s,
+            "unit": UNIT,
+            "h2d_bytes_per_step": (h1 - h0) / args.e2e_steps,
+            "d2h_bytes_per_step": (d1b - d0b) / args.e2e_steps,
+            "how": "C ABI synq_sim_run(10000) with recording + synq_sim_raster_copy into host "
+                   "numpy buffers per step, wall clock",
+            "raster_bytes_last_step": raster_bytes_host,
+        },
+        "clocks": clocks.summary(),
+    }
+    if cpu_thread is not None:
+        cpu_thread.join()
+        if "error" in cpu_result:
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": "failed: " + cpu_result["error"]}
+        else:
+            v = cpu_result["events"] / cpu_result["sim_s"]
+            line["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"{cpu_result['steps']} timesteps (after 200 warm-up) of the same Brunel "
+                          f"1e9 network ({cpu_result['synapses']} synapses), reference deterministic "
+                          f"mode, 1 thread; construction {cpu_result['construct_s']:.1f} s",
+                "wall_s_per_bio_s": cpu_result["sim_s"] * BIO_STEPS / cpu_result["steps"],
+            }
+    print(json.dumps(line))
+    sim.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

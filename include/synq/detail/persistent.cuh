@@ -61,9 +61,12 @@ struct persist_state {
     uint32_t* step_spikes;
     uint32_t* step_meas;
     uint32_t meas_lo, meas_hi;
-    unsigned long long* log;  // (t << 32 | id), only when recording
-    unsigned long long* log_cursor;
+    // ordered frame log (recording / taps): CTA 0 copies every frame it
+    // receives with due >= log_from, in CTA (= ascending id) order
+    uint32_t* log;
+    unsigned long long* log_end;  // out: entries written
     unsigned long long log_cap;
+    int64_t log_from;
     uint32_t* flags;
     uint32_t win_cap;      // count-window capacity per class (smem)
     uint32_t spike_chunk;  // spikes staged per receive round (smem)
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     __shared__ uint32_t s_lo[kMaxTiles + 1];
     __shared__ uint32_t s_seg[kMaxTiles + 1];
     __shared__ uint32_t s_warp[NW];
-    __shared__ uint32_t s_pass, s_meas, s_logbase;
+    __shared__ uint32_t s_pass, s_meas;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t c = blockIdx.x, C = ps.C;
@@ -113,6 +116,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     const uint32_t lo = s_lo[c], hi = s_lo[c + 1];
     const uint32_t wlo = ps.win_lo[c];
     unsigned long long my_deliv = 0, my_spikes = 0;
+    unsigned long long lc = 0;  // CTA 0: log cursor
 
     for (int32_t s = 0; s < nsteps; ++s) {
         const int64_t t = t0 + s;
@@ -180,18 +184,8 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
             if (s_meas) atomicAdd(&ps.step_meas[s], s_meas);
             s_meas = 0;
             my_spikes += out;
-            if (ps.log && out) {
-                const unsigned long long b = atomicAdd(ps.log_cursor, static_cast<unsigned long long>(out));
-                s_logbase = static_cast<uint32_t>(b < ps.log_cap ? b : ps.log_cap);
-                if (b + out > ps.log_cap) ps.flags[0] = 1;
-            }
         }
-        if (ps.log && out) {
-            __syncthreads();
-            const unsigned long long b = s_logbase;
-            for (uint32_t j = tid; j < out && b + j < ps.log_cap; j += NT)
-                ps.log[b + j] = (static_cast<unsigned long long>(t) << 32) | qseg[j];
-        }
+        __syncthreads();
 
         // ------------------------------------------------ Receive(t - delay + 1)
         const int64_t due = t - static_cast<int64_t>(ps.delay) + 1;
@@ -225,6 +219,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         __syncthreads();
         const uint32_t S = s_seg[C];
         const uint32_t* dq = ps.queue + static_cast<uint64_t>(dslot) * ps.n;
+        const bool logging = ps.log && c == 0 && due >= ps.log_from;
         for (uint32_t c0 = 0; c0 < S; c0 += ps.spike_chunk) {
             const uint32_t m = min(ps.spike_chunk, S - c0);
             // stage ids and this tile's row segments
@@ -238,6 +233,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                 const uint32_t src = __ldcg(dq + s_lo[a] + (gg - s_seg[a]));
                 const uint32_t* sp = ps.split + static_cast<uint64_t>(src) * (C + 1) + c;
                 const uint32_t sb = __ldg(sp), se = __ldg(sp + 1);
+                if (logging && lc + gg < ps.log_cap) ps.log[lc + gg] = src;
                 s_src[g] = src;
                 s_beg[g] = sb;
                 s_len[g] = se - sb;
@@ -274,6 +270,11 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
             }
             __syncthreads();
         }
+        if (logging) lc += S;
+    }
+    if (ps.log && c == 0 && tid == 0) {
+        *ps.log_end = lc;
+        if (lc > ps.log_cap) ps.flags[0] = 1;
     }
 
     // fold pending arrivals into ACC so host reads and the next launch see them
@@ -292,6 +293,42 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     for (int o = 16; o; o >>= 1) my_deliv += __shfl_xor_sync(0xffffffffu, my_deliv, o);
     if (lane == 0 && my_deliv) atomicAdd(&ps.counters[C_DELIVERIES], my_deliv);
     if (tid == 0 && my_spikes) atomicAdd(&ps.counters[C_SPIKES], my_spikes);
+}
+
+// Copy frames [from, to] (all complete in the ring) into the ordered log;
+// used once at the end of run() for the frames not yet consumed by Receive.
+template <class M>
+__global__ void k_log_drain(persist_state<M> ps, int64_t from, int64_t to) {
+    __shared__ uint32_t s_seg[kMaxTiles + 1];
+    __shared__ uint32_t s_lo[kMaxTiles + 1];
+    const uint32_t C = ps.C;
+    for (uint32_t j = threadIdx.x; j <= C; j += blockDim.x) s_lo[j] = ps.tile_lo[j];
+    unsigned long long lc = 0;
+    for (int64_t f = from; f <= to; ++f) {
+        const uint32_t slot = static_cast<uint32_t>(f % ps.Q);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t run = 0;
+            for (uint32_t j = 0; j < C; ++j) {
+                s_seg[j] = run;
+                run += static_cast<uint32_t>(ps.finfo[static_cast<uint64_t>(slot) * C + j]);
+            }
+            s_seg[C] = run;
+        }
+        __syncthreads();
+        const uint32_t S = s_seg[C];
+        for (uint32_t j = 0; j < C; ++j) {
+            const uint32_t cnt = s_seg[j + 1] - s_seg[j];
+            for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x)
+                if (lc + s_seg[j] + k < ps.log_cap)
+                    ps.log[lc + s_seg[j] + k] = ps.queue[static_cast<uint64_t>(slot) * ps.n + s_lo[j] + k];
+        }
+        lc += S;
+    }
+    if (threadIdx.x == 0) {
+        *ps.log_end = lc;
+        if (lc > ps.log_cap) ps.flags[0] = 1;
+    }
 }
 
 }  // namespace synq::dev

@@ -152,6 +152,7 @@ public:
         int dev = 0;
         SYNQ_CUDA(cudaGetDevice(&dev));
         SYNQ_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev));
+        for (auto& e : ev_) SYNQ_CUDA(cudaEventCreate(&e));
 
         auto t0 = clock::now();
         graph_ = build_device_graph(desc_, opt_.seed, opt_.pitch_align, stream_);
@@ -169,6 +170,8 @@ public:
 
     ~network() {
         if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+        for (auto& e : ev_)
+            if (e) cudaEventDestroy(e);
         if (stream_) {
             cudaStreamSynchronize(stream_);
             cudaStreamDestroy(stream_);
@@ -186,6 +189,7 @@ public:
         step_measured_.clear();
         step_spikes_host_.clear();
         expiring_host_.clear();
+        logged_upto_ = 0;
         const int64_t zero = 0;
         SYNQ_CUDA(cudaMemcpyAsync(t_dev_.get(), &zero, sizeof zero, cudaMemcpyHostToDevice, stream_));
         counters_dev_.zero(stream_);
@@ -230,11 +234,18 @@ public:
         if (steps <= 0) return;
         push_mirrors();
         auto t0 = clock::now();
+        SYNQ_CUDA(cudaEventRecord(ev_[0], stream_));
         while (steps > 0) {
             const int64_t b = std::min<int64_t>(steps, batch_cap_);
             run_batch(static_cast<uint32_t>(b));
             steps -= b;
         }
+        if (persistent_ && log_ids_ && logged_upto_ < t_) drain_log();
+        SYNQ_CUDA(cudaEventRecord(ev_[1], stream_));
+        SYNQ_CUDA(cudaEventSynchronize(ev_[1]));
+        float ms = 0;
+        SYNQ_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+        device_seconds_ += ms * 1e-3;
         timings_.simulate += since(t0);
         invalidate_mirrors();
     }
@@ -274,10 +285,22 @@ public:
     bool persistent() const { return persistent_; }
     bool exact() const { return exact_ || persistent_; }
     uint64_t construction_fixups() const { return graph_.tie_fixups; }
+    // device time of all run() calls (CUDA events on the engine stream) and of
+    // the dominant kernel alone; kernel launches; host<->device bytes moved
+    double device_seconds() const { return device_seconds_; }
+    double kernel_seconds() const { return kernel_seconds_; }
+    uint64_t kernel_launches() const { return launches_; }
+    uint64_t h2d_bytes() const { return h2d_bytes_; }
+    uint64_t d2h_bytes() const { return d2h_bytes_; }
 
     void set_spike_tap(tap_fn fn) {
         tap_ = std::move(fn);
-        ensure_log();
+        if (tap_) {
+            ensure_log();
+            logged_upto_ = t_;  // a new tap observes frames from now on
+        } else {
+            drop_log();
+        }
     }
 
     // measured-population spike counts per step, kept on the device and
@@ -467,18 +490,26 @@ private:
         graph_exec_ = nullptr;
     }
 
+    void drop_log() {
+        if (!log_ids_) return;
+        reset_graph();
+        log_ids_ = dev_array<uint32_t>();
+        log_cap_ = 0;
+    }
+
     void ensure_log() {
-        if (log_ids_ || log_pairs_) return;
+        if (log_ids_) return;
         reset_graph();
         // frames of one batch; the batch shrinks to keep the log bounded
-        const uint64_t cap = std::max<uint64_t>(1024, std::min<uint64_t>(uint64_t(batch_cap_) * n_, 1ull << 26));
-        if (persistent_)
-            log_pairs_.resize(cap);
-        else
-            log_ids_.resize(cap);
+        const uint64_t cap = std::max<uint64_t>(1024, std::min<uint64_t>(uint64_t(batch_cap_ + delay_) * n_, 1ull << 26));
+        log_ids_.resize(cap);
+        log_end_.resize(1);
         log_cap_ = cap;
         log_host_.resize(cap);
-        if (uint64_t(batch_cap_) * n_ > cap) batch_cap_ = std::max<uint32_t>(1, static_cast<uint32_t>(cap / std::max<uint32_t>(1, n_)));
+        // a persistent batch logs up to delay-1 frames of the previous batch too
+        const uint64_t frames = cap / std::max<uint32_t>(1, n_);
+        const uint64_t fit = frames > delay_ ? frames - delay_ : 1;
+        batch_cap_ = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(batch_cap_, fit)));
     }
 
     dev::engine_state<Model> state() {
@@ -550,9 +581,10 @@ private:
         p.step_meas = step_meas_dev_.get();
         p.meas_lo = meas_lo_;
         p.meas_hi = meas_hi_;
-        p.log = log_pairs_.get();
-        p.log_cursor = log_cursor_.get();
+        p.log = log_ids_.get();
+        p.log_end = log_end_.get();
         p.log_cap = log_cap_;
+        p.log_from = logged_upto_;
         p.flags = flags_.get();
         p.win_cap = win_cap_;
         p.spike_chunk = spike_chunk_;
@@ -593,9 +625,13 @@ private:
     void run_batch(uint32_t b) {
         step_spikes_dev_.zero(stream_);
         step_meas_dev_.zero(stream_);
-        const unsigned long long zero2[2] = {0, 0};
-        if (log_ids_ || log_pairs_)
+        const bool logging = static_cast<bool>(log_ids_);
+        if (logging && !persistent_) {
+            const unsigned long long zero2[2] = {0, 0};
             SYNQ_CUDA(cudaMemcpyAsync(log_cursor_.get(), zero2, sizeof zero2, cudaMemcpyHostToDevice, stream_));
+            h2d_bytes_ += sizeof zero2;
+        }
+        SYNQ_CUDA(cudaEventRecord(ev_[2], stream_));
         if (persistent_) {
             if constexpr (population_model) {
                 auto ps = pstate();
@@ -606,10 +642,12 @@ private:
                 SYNQ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_persistent<Model>),
                                                       dim3(tiles_), dim3(dev::kPersistThreads), args,
                                                       smem_, stream_));
+                launches_ += 1;
             }
         } else {
             const int64_t t0 = t_;
             SYNQ_CUDA(cudaMemcpyAsync(t0_dev_.get(), &t0, sizeof t0, cudaMemcpyHostToDevice, stream_));
+            h2d_bytes_ += sizeof t0;
             uint32_t left = b;
             if (left >= kGraphSteps) {
                 ensure_graph();
@@ -619,23 +657,30 @@ private:
                 }
             }
             while (left--) enqueue_generic_step();
+            launches_ += uint64_t(b) * kernels_per_step();
         }
         SYNQ_CUDA(cudaGetLastError());
+        SYNQ_CUDA(cudaEventRecord(ev_[3], stream_));
         step_spikes_dev_.download(step_buf_.data(), b, stream_);
         step_meas_dev_.download(step_buf_.data() + b, b, stream_);
+        d2h_bytes_ += 8ull * b;
         uint64_t logged = 0;
-        if (log_ids_ || log_pairs_) {
-            unsigned long long cur[2];
-            SYNQ_CUDA(cudaMemcpyAsync(cur, log_cursor_.get(), sizeof cur, cudaMemcpyDeviceToHost, stream_));
+        if (logging) {
+            unsigned long long cur[2] = {0, 0};
+            if (persistent_)
+                SYNQ_CUDA(cudaMemcpyAsync(cur, log_end_.get(), sizeof(cur[0]), cudaMemcpyDeviceToHost, stream_));
+            else
+                SYNQ_CUDA(cudaMemcpyAsync(cur, log_cursor_.get(), sizeof cur, cudaMemcpyDeviceToHost, stream_));
             SYNQ_CUDA(cudaStreamSynchronize(stream_));
             logged = persistent_ ? cur[0] : cur[(t_ + b) & 1];
             logged = std::min<uint64_t>(logged, log_cap_);
-            if (persistent_)
-                log_pairs_.download(log_host_.data(), logged, stream_);
-            else
-                log_ids_.download(reinterpret_cast<uint32_t*>(log_host_.data()), logged, stream_);
+            log_ids_.download(log_host_.data(), logged, stream_);
+            d2h_bytes_ += 16 + 4 * logged;
         }
         pull_counters();  // synchronises
+        float ms = 0;
+        SYNQ_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+        kernel_seconds_ += ms * 1e-3;
         if (flags_host_[0]) throw device_error("spike log overflow (batch too large for the frame log)");
         if (flags_host_[1]) throw device_error("ordered delivery scratch overflow");
 
@@ -646,31 +691,46 @@ private:
             if (t_ + k - int64_t(delay_) + 1 >= 0) ++counters_.frames_consumed;
         }
         counters_.steps += b;
-        if (log_ids_ || log_pairs_) replay_taps(b, logged);
-        t_ += b;
+        const int64_t t_end = t_ + b;
+        if (logging) {
+            // generic: frames t_ .. t_end-1; persistent: frames logged_upto_ .. t_end-delay
+            const int64_t last = persistent_ ? t_end - int64_t(delay_) : t_end - 1;
+            emit_logged(logged, last);
+        }
+        t_ = t_end;
     }
 
-    void replay_taps(uint32_t b, uint64_t logged) {
+    uint64_t kernels_per_step() const {
+        return 2 + (has_synapses ? 1 : 0) + (exact_ ? 3 : 0);
+    }
+
+    // frames logged_upto_ .. last are the next entries of log_host_, in order
+    void emit_logged(uint64_t logged, int64_t last) {
         std::vector<uint32_t> frame;
-        if (persistent_) {
-            unsigned long long* p = log_host_.data();
-            std::sort(p, p + logged);
-            uint64_t q = 0;
-            for (uint32_t k = 0; k < b; ++k) {
-                const int64_t t = t_ + k;
-                frame.clear();
-                while (q < logged && static_cast<int64_t>(p[q] >> 32) == t) frame.push_back(uint32_t(p[q++]));
-                emit(t, frame);
-            }
-        } else {
-            const uint32_t* ids = reinterpret_cast<const uint32_t*>(log_host_.data());
-            uint64_t off = 0;
-            for (uint32_t k = 0; k < b; ++k) {
-                const uint32_t cnt = step_buf_[k];
-                frame.assign(ids + off, ids + std::min<uint64_t>(off + cnt, logged));
-                off += cnt;
-                emit(t_ + k, frame);
-            }
+        uint64_t off = 0;
+        for (int64_t f = logged_upto_; f <= last; ++f) {
+            const uint32_t cnt = step_spikes_host_[static_cast<size_t>(f)];
+            frame.assign(log_host_.data() + std::min(off, logged), log_host_.data() + std::min(off + cnt, logged));
+            off += cnt;
+            emit(f, frame);
+        }
+        logged_upto_ = std::max(logged_upto_, last + 1);
+    }
+
+    void drain_log() {
+        if constexpr (population_model) {
+            auto ps = pstate();
+            dev::k_log_drain<Model><<<1, 1024, 0, stream_>>>(ps, logged_upto_, t_ - 1);
+            SYNQ_CUDA(cudaGetLastError());
+            launches_ += 1;
+            unsigned long long end = 0;
+            SYNQ_CUDA(cudaMemcpyAsync(&end, log_end_.get(), sizeof end, cudaMemcpyDeviceToHost, stream_));
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            const uint64_t logged = std::min<uint64_t>(end, log_cap_);
+            log_ids_.download(log_host_.data(), logged, stream_);
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            d2h_bytes_ += 8 + 4 * logged;
+            emit_logged(logged, t_ - 1);
         }
     }
 
@@ -686,6 +746,7 @@ private:
         counters_dev_.download(c, dev::C_COUNT, stream_);
         flags_.download(flags_host_, 4, stream_);
         SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        d2h_bytes_ += sizeof c + sizeof flags_host_;
         counters_.spikes = c[dev::C_SPIKES];
         counters_.deliveries = c[dev::C_DELIVERIES];
         counters_.synapse_updates = c[dev::C_SYN_UPDATES];
@@ -759,8 +820,12 @@ private:
     dev_array<unsigned long long> det_ev_;
     uint64_t det_cap_ = 0;
     dev_array<uint32_t> log_ids_;
-    dev_array<unsigned long long> log_pairs_;
-    pinned_array<unsigned long long> log_host_;
+    dev_array<unsigned long long> log_end_;
+    pinned_array<uint32_t> log_host_;
+    int64_t logged_upto_ = 0;
+    cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
+    double device_seconds_ = 0, kernel_seconds_ = 0;
+    uint64_t launches_ = 0, h2d_bytes_ = 0, d2h_bytes_ = 0;
     uint64_t log_cap_ = 0;
     uint32_t flags_host_[4] = {0, 0, 0, 0};
     cudaGraphExec_t graph_exec_ = nullptr;

@@ -125,6 +125,10 @@ def lib() -> C.CDLL:
     sig("synq_sim_graph_shape", st, vp, C.POINTER(u32), C.POINTER(u32))
     sig("synq_sim_graph_cells", st, vp, vp, u64)
     sig("synq_sim_construction_fixups", u64, vp)
+    sig("synq_sim_device_time", st, vp, vp)
+    sig("synq_sim_kernel_launches", u64, vp)
+    sig("synq_sim_transfer_bytes", st, vp, vp)
+    sig("synq_sim_set_record", st, vp, C.c_int)
     _lib = L
     return L
 
@@ -327,6 +331,23 @@ class Sim:
 
     def construction_fixups(self) -> int:
         return int(lib().synq_sim_construction_fixups(self.h))
+
+    def device_time(self):
+        """(device seconds of run/step, seconds inside the step kernels)"""
+        out = np.zeros(2, np.float64)
+        check(lib().synq_sim_device_time(self.h, _p(out)))
+        return float(out[0]), float(out[1])
+
+    def set_record(self, on: bool):
+        check(lib().synq_sim_set_record(self.h, int(on)))
+
+    def kernel_launches(self) -> int:
+        return int(lib().synq_sim_kernel_launches(self.h))
+
+    def transfer_bytes(self):
+        out = np.zeros(2, np.uint64)
+        check(lib().synq_sim_transfer_bytes(self.h, _p(out)))
+        return int(out[0]), int(out[1])
 
 
 def memory_estimate(model: str, neurons: int, synapses: int) -> dict:

@@ -65,6 +65,10 @@ public:
     virtual void synapse_field_bytes(uint32_t f, void* out, uint64_t bytes) = 0;
     virtual const adjacency_list& graph() const = 0;
     virtual uint64_t fixups() const = 0;
+    virtual void device_time(double out[2]) const = 0;
+    virtual uint64_t launches() const = 0;
+    virtual void transfers(uint64_t out[2]) const = 0;
+    virtual void set_record(bool on) = 0;
 
     void write_stats(std::ostream& out) const;
     void write_stats_to(const std::string& path) const;
@@ -117,10 +121,18 @@ public:
         net_->set_measure_range(mb_, me_);
         raster_.dt = net_->dt();
         raster_.neurons = net_->neuron_count();
-        if (record_)
+        if (record_) set_record(true);
+    }
+
+    void set_record(bool on) override {
+        record_ = on;
+        raster_.records.clear();
+        if (on)
             net_->set_spike_tap([this](int64_t t, std::span<const uint32_t> frame) {
                 for (uint32_t id : frame) raster_.records.push_back({t, id});
             });
+        else
+            net_->set_spike_tap(nullptr);
     }
 
     void step() override { net_->step(); }
@@ -170,6 +182,15 @@ public:
     }
     const adjacency_list& graph() const override { return net_->graph(); }
     uint64_t fixups() const override { return net_->construction_fixups(); }
+    void device_time(double out[2]) const override {
+        out[0] = net_->device_seconds();
+        out[1] = net_->kernel_seconds();
+    }
+    uint64_t launches() const override { return net_->kernel_launches(); }
+    void transfers(uint64_t out[2]) const override {
+        out[0] = net_->h2d_bytes();
+        out[1] = net_->d2h_bytes();
+    }
 
 private:
     model_kind kind_;
@@ -697,5 +718,26 @@ synq_status synq_sim_graph_cells(const synq_sim* s, uint32_t* out, uint64_t capa
     });
 }
 uint64_t synq_sim_construction_fixups(const synq_sim* s) { return s ? s->impl->fixups() : 0; }
+
+synq_status synq_sim_device_time(const synq_sim* s, double out[2]) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(out);
+    s->impl->device_time(out);
+    return SYNQ_OK;
+}
+uint64_t synq_sim_kernel_launches(const synq_sim* s) { return s ? s->impl->launches() : 0; }
+synq_status synq_sim_set_record(synq_sim* s, int on) {
+    SYNQ_CHECK_HANDLE(s);
+    return guarded([&] {
+        s->impl->set_record(on != 0);
+        return SYNQ_OK;
+    });
+}
+synq_status synq_sim_transfer_bytes(const synq_sim* s, uint64_t out[2]) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(out);
+    s->impl->transfers(out);
+    return SYNQ_OK;
+}
 
 }  // extern "C"
