@@ -63,6 +63,7 @@ struct engine_options {
     uint32_t batch_steps = 0;  // steps per device batch (0 = auto)
     int persistent = -1;       // -1 auto, 0 never, 1 require (population-delivery models)
     uint32_t tiles = 0;        // persistent CTAs (0 = auto)
+    bool profile = false;      // per-phase cycle counters in the persistent kernel
 };
 
 struct engine_counters {
@@ -292,6 +293,32 @@ public:
     uint64_t kernel_launches() const { return launches_; }
     uint64_t h2d_bytes() const { return h2d_bytes_; }
     uint64_t d2h_bytes() const { return d2h_bytes_; }
+    unsigned tiles() const { return tiles_; }
+    // persistent-kernel phase profile: average cycles per step per CTA for
+    // update, publish, poll, gather, deliver (opt.profile only)
+    std::vector<double> phase_cycles() const {
+        // [0..4] mean over CTAs, [5..9] the pacing CTA (least time waiting for
+        // its staged frame); slots: update, publish, wait, deliver, producer prep
+        std::vector<double> out(15, 0.0);
+        if (!prof_ || !tiles_) return out;
+        std::vector<unsigned long long> h(prof_.size());
+        prof_.download(h.data(), h.size(), stream_);
+        SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        uint32_t crit = 0;
+        double best = 1e300;
+        for (uint32_t c = 0; c < tiles_; ++c) {
+            const double steps = std::max<unsigned long long>(1, h[c * dev::P_SLOTS + dev::P_STEPS]);
+            for (int k = 0; k < 5; ++k) out[k] += h[c * dev::P_SLOTS + k] / steps / tiles_;
+            const double poll = h[c * dev::P_SLOTS + dev::P_POLL] / steps;
+            if (poll < best) {
+                best = poll;
+                crit = c;
+            }
+        }
+        const double steps = std::max<unsigned long long>(1, h[crit * dev::P_SLOTS + dev::P_STEPS]);
+        for (int k = 0; k < 5; ++k) out[5 + k] = h[crit * dev::P_SLOTS + k] / steps;
+        return out;
+    }
 
     void set_spike_tap(tap_fn fn) {
         tap_ = std::move(fn);
@@ -425,62 +452,103 @@ private:
         step_buf_.resize(2 * size_t(batch_cap_));
     }
 
+    // Partition for the persistent engine (detail/persistent.cuh): every CTA
+    // owns a receiving piece A_c and an update-only piece B_c; pieces tile the
+    // id space and are numbered in id order.
     void setup_persistent() requires population_model {
         const std::vector<uint32_t> indeg = in_degrees(graph_, stream_);
-        uint32_t C = opt_.tiles ? opt_.tiles
-                                : static_cast<uint32_t>(std::clamp<int64_t>(
-                                      (static_cast<int64_t>(n_) + 511) / 1024, 1, sms_));
-        C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), std::max<uint32_t>(1, n_)});
-        // cost per neuron: a fixed update share plus expected arrivals
-        std::vector<double> prefix(size_t(n_) + 1, 0.0);
-        for (uint32_t i = 0; i < n_; ++i) prefix[i + 1] = prefix[i] + 16.0 + 0.003 * indeg[i];
-        std::vector<uint32_t> lo(C + 1, n_);
-        lo[0] = 0;
-        for (uint32_t c = 1; c < C; ++c) {
-            const double target = prefix[n_] * c / C;
-            lo[c] = static_cast<uint32_t>(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
-            lo[c] = std::clamp(lo[c], lo[c - 1], n_);
-        }
-        lo[C] = n_;
-        std::vector<uint32_t> wlo(C);
-        uint32_t wcap = 1;
-        for (uint32_t c = 0; c < C; ++c) {
-            uint32_t a = lo[c], b = lo[c + 1];
-            while (a < b && indeg[a] == 0) ++a;
-            while (b > a && indeg[b - 1] == 0) --b;
-            wlo[c] = a < b ? a : lo[c + 1];
-            wcap = std::max(wcap, b - a);
-        }
         uint32_t bound[dev::kMaxClasses] = {};
         float delta[dev::kMaxClasses] = {};
         const int K = population_delivery<Model>::classes(model_, n_, bound, delta);
-        const size_t spike_chunk = 1024;
-        const size_t smem = (size_t(K) * wcap + 3 * spike_chunk) * sizeof(uint32_t);
+        if (K < 1 || K > dev::kMaxClasses || n_ == 0) return;
+        // receiving region [r0, r1): everything outside receives nothing
+        uint32_t r0 = 0, r1 = 0;
+        while (r0 < n_ && indeg[r0] == 0) ++r0;
+        r1 = n_;
+        while (r1 > r0 && indeg[r1 - 1] == 0) --r1;
+        if (r0 == r1) r0 = r1 = 0;
+        // the update-only remainder must be one range on one side, else the
+        // whole id space is the receiving region (B pieces stay empty)
+        uint32_t u0 = r1, u1 = n_;
+        bool u_after = true;
+        if (r0 > 0 && r1 < n_) {
+            r0 = 0;
+            r1 = n_;
+            u0 = u1 = n_;
+        } else if (r0 > 0) {
+            u0 = 0;
+            u1 = r0;
+            u_after = false;
+        }
+        const uint32_t nr = r1 - r0, nu = u1 - u0;
+        const uint32_t NTH = dev::kPersistThreads;
+        uint32_t C = opt_.tiles ? opt_.tiles
+                                : static_cast<uint32_t>(std::clamp<int64_t>(
+                                      (static_cast<int64_t>(n_) + NTH / 2) / NTH, 1, sms_));
+        C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), n_});
+        const uint32_t max_local = 4 * NTH;  // register-resident state: <= 4 neurons per thread
+        if (uint64_t(C) * max_local < n_) C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (n_ + max_local - 1) / max_local));
+        // A pieces by receive cost (update share + expected arrivals), B by count
+        std::vector<double> prefix(size_t(nr) + 1, 0.0);
+        for (uint32_t k = 0; k < nr; ++k) prefix[k + 1] = prefix[k] + 16.0 + 0.003 * indeg[r0 + k];
+        std::vector<uint32_t> alo(C + 1), blo(C + 1);
+        for (uint32_t c = 0; c <= C; ++c) {
+            const double target = prefix[nr] * c / C;
+            alo[c] = r0 + static_cast<uint32_t>(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
+            blo[c] = u0 + static_cast<uint32_t>(uint64_t(nu) * c / C);
+        }
+        alo[0] = r0;
+        alo[C] = r1;
+        for (uint32_t c = 1; c <= C; ++c) alo[c] = std::max(alo[c], alo[c - 1]);
+        uint32_t longest = 0, wcap = 1;
+        for (uint32_t c = 0; c < C; ++c) {
+            longest = std::max(longest, (alo[c + 1] - alo[c]) + (blo[c + 1] - blo[c]));
+            wcap = std::max(wcap, alo[c + 1] - alo[c]);
+        }
+        if (longest > max_local) return;  // cannot hold the state: per-step kernel graph
+        npt_ = longest <= NTH ? 1 : (longest <= 2 * NTH ? 2 : 4);
+        // pieces in id order
+        const uint32_t P = 2 * C;
+        std::vector<uint32_t> piece_lo(P + 1), cta_piece(2 * C);
+        for (uint32_t c = 0; c < C; ++c) {
+            const uint32_t ia = u_after ? c : C + c, ib = u_after ? C + c : c;
+            piece_lo[ia] = alo[c];
+            piece_lo[ib] = blo[c];
+            cta_piece[2 * c] = ia;
+            cta_piece[2 * c + 1] = ib;
+        }
+        piece_lo[P] = n_;
+        // dynamic smem: counts only (delivery items are static)
         int max_smem = 0, dev = 0;
         SYNQ_CUDA(cudaGetDevice(&dev));
         SYNQ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const size_t static_smem = (2 * (dev::kMaxTiles + 1) + 64) * sizeof(uint32_t);
-        if (K < 1 || K > dev::kMaxClasses || smem + static_smem > size_t(max_smem)) return;
-        SYNQ_CUDA(cudaFuncSetAttribute(dev::k_persistent<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
+        const size_t static_smem = (dev::kItemCap + dev::kItemBatch * 32) * 16 + 3 * (dev::kMaxPieces + 1) * 4 + 8192;
+        const size_t smem = ((size_t(K) * wcap + 3) & ~size_t(3)) * 4;
+        if (smem + static_smem > size_t(max_smem)) return;
+        npt_select_ = npt_;
+        const void* fn = persistent_fn();
+        SYNQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
-        SYNQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_persistent<Model>,
-                                                                dev::kPersistThreads, smem));
+        SYNQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, dev::kPersistThreads, smem));
         if (per_sm < 1) return;
+        if (opt_.profile) {
+            prof_.resize(size_t(C) * dev::P_SLOTS);
+            prof_.zero(stream_);
+        }
 
         tiles_ = C;
-        tile_lo_host_ = lo;
-        tile_lo_.resize(C + 1);
-        tile_lo_.upload(lo.data(), C + 1, stream_);
-        win_lo_.resize(C);
-        win_lo_.upload(wlo.data(), C, stream_);
-        build_splits(graph_, lo, split_, stream_);
-        finfo_.resize(size_t(2) * delay_ * C);
+        pieces_ = P;
+        tile_lo_host_ = piece_lo;
+        tile_lo_.resize(P + 1);
+        tile_lo_.upload(piece_lo.data(), P + 1, stream_);
+        win_lo_.resize(2 * C);
+        win_lo_.upload(cta_piece.data(), 2 * C, stream_);
+        build_splits(graph_, alo, split_, stream_);
+        finfo_.resize(size_t(2) * delay_ * P);
         K_ = K;
         std::copy(bound, bound + dev::kMaxClasses, bound_);
         std::copy(delta, delta + dev::kMaxClasses, delta_);
         win_cap_ = wcap;
-        spike_chunk_ = spike_chunk;
         smem_ = smem;
         persistent_ = true;
     }
@@ -557,17 +625,26 @@ private:
         return s;
     }
 
+    const void* persistent_fn() const requires population_model {
+        switch (npt_) {
+            case 1: return reinterpret_cast<const void*>(dev::k_persistent<Model, 1>);
+            case 2: return reinterpret_cast<const void*>(dev::k_persistent<Model, 2>);
+            default: return reinterpret_cast<const void*>(dev::k_persistent<Model, 4>);
+        }
+    }
+
     dev::persist_state<Model> pstate() requires population_model {
         dev::persist_state<Model> p{};
         p.nf = nptrs_;
         p.rng = rng_.get();
         p.cells = graph_.cells.get();
         p.split = split_.get();
-        p.tile_lo = tile_lo_.get();
-        p.win_lo = win_lo_.get();
+        p.piece_lo = tile_lo_.get();
+        p.cta_piece = win_lo_.get();
         p.pitch = graph_.pitch;
         p.n = n_;
         p.C = tiles_;
+        p.P = pieces_;
         p.queue = queue_.get();
         p.finfo = finfo_.get();
         p.Q = Q_;
@@ -587,7 +664,7 @@ private:
         p.log_from = logged_upto_;
         p.flags = flags_.get();
         p.win_cap = win_cap_;
-        p.spike_chunk = spike_chunk_;
+        p.prof = prof_ ? prof_.get() : nullptr;
         return p;
     }
 
@@ -639,9 +716,8 @@ private:
                 int32_t nsteps = static_cast<int32_t>(b);
                 Model m = model_;
                 void* args[] = {&m, &ps, &t0, &nsteps};
-                SYNQ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_persistent<Model>),
-                                                      dim3(tiles_), dim3(dev::kPersistThreads), args,
-                                                      smem_, stream_));
+                SYNQ_CUDA(cudaLaunchCooperativeKernel(persistent_fn(), dim3(tiles_),
+                                                      dim3(dev::kPersistThreads), args, smem_, stream_));
                 launches_ += 1;
             }
         } else {
@@ -840,8 +916,11 @@ private:
     int K_ = 0;
     uint32_t bound_[dev::kMaxClasses] = {};
     float delta_[dev::kMaxClasses] = {};
-    uint32_t win_cap_ = 0, spike_chunk_ = 0;
+    uint32_t win_cap_ = 0, pieces_ = 0;
+    int npt_select_ = 1;
     size_t smem_ = 0;
+    int npt_ = 1;
+    dev_array<unsigned long long> prof_;
 
     // host-visible state
     neuron_store host_neurons_;

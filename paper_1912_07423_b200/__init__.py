@@ -17,7 +17,7 @@ import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libsynq.so.1")
+LIB_PATH = os.environ.get("SYNQ_LIB") or os.path.join(PKG_DIR, "lib", "libsynq.so.1")
 HEADER = os.path.join(ROOT, "include", "synq", "synq.h")
 
 SYNQ_OK = 0
@@ -129,6 +129,8 @@ def lib() -> C.CDLL:
     sig("synq_sim_kernel_launches", u64, vp)
     sig("synq_sim_transfer_bytes", st, vp, vp)
     sig("synq_sim_set_record", st, vp, C.c_int)
+    sig("synq_opts_profile", st, vp, C.c_int)
+    sig("synq_sim_phase_cycles", st, vp, vp, C.POINTER(u32))
     _lib = L
     return L
 
@@ -147,7 +149,7 @@ class Opts:
 
     def __init__(self, seed=None, threads=None, deterministic=None, dt=None, delay=None,
                  record=None, defaults_file=None, params=None, batch_steps=None,
-                 persistent=None, tiles=None):
+                 persistent=None, tiles=None, profile=None):
         self.h = lib().synq_opts_new()
         if not self.h:
             raise MemoryError("synq_opts_new")
@@ -174,6 +176,8 @@ class Opts:
             check(L.synq_opts_persistent(self.h, persistent))
         if tiles is not None:
             check(L.synq_opts_tiles(self.h, tiles))
+        if profile is not None:
+            check(L.synq_opts_profile(self.h, int(profile)))
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -337,6 +341,17 @@ class Sim:
         out = np.zeros(2, np.float64)
         check(lib().synq_sim_device_time(self.h, _p(out)))
         return float(out[0]), float(out[1])
+
+    def phase_cycles(self) -> dict:
+        out = np.zeros(15, np.float64)
+        tiles = C.c_uint32()
+        check(lib().synq_sim_phase_cycles(self.h, _p(out), C.byref(tiles)))
+        names = ["update", "publish", "poll", "gather", "deliver"]
+        d = {"mean": dict(zip(names, (round(float(x)) for x in out[:5]))),
+             "pacing": dict(zip(names, (round(float(x)) for x in out[5:10]))),
+             "producer": dict(zip(["poll", "ids", "splits", "rebase", "issue"],
+                                  (round(float(x)) for x in out[10:15]))), "tiles": tiles.value}
+        return d
 
     def set_record(self, on: bool):
         check(lib().synq_sim_set_record(self.h, int(on)))

@@ -69,6 +69,8 @@ public:
     virtual uint64_t launches() const = 0;
     virtual void transfers(uint64_t out[2]) const = 0;
     virtual void set_record(bool on) = 0;
+    virtual std::vector<double> phase_cycles() const = 0;
+    virtual unsigned tiles() const = 0;
 
     void write_stats(std::ostream& out) const;
     void write_stats_to(const std::string& path) const;
@@ -124,6 +126,8 @@ public:
         if (record_) set_record(true);
     }
 
+    std::vector<double> phase_cycles() const override { return net_->phase_cycles(); }
+    unsigned tiles() const override { return net_->tiles(); }
     void set_record(bool on) override {
         record_ = on;
         raster_.records.clear();
@@ -634,6 +638,21 @@ synq_status synq_opts_tiles(synq_opts* o, uint32_t tiles) {
     SYNQ_CHECK_HANDLE(o);
     o->cfg.engine.tiles = tiles;
     return SYNQ_OK;
+}
+synq_status synq_opts_profile(synq_opts* o, int on) {
+    SYNQ_CHECK_HANDLE(o);
+    o->cfg.engine.profile = on != 0;
+    return SYNQ_OK;
+}
+synq_status synq_sim_phase_cycles(const synq_sim* s, double out[15], uint32_t* tiles) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(out);
+    return guarded([&] {
+        const auto v = s->impl->phase_cycles();
+        for (int k = 0; k < 15; ++k) out[k] = v[k];
+        if (tiles) *tiles = s->impl->tiles();
+        return SYNQ_OK;
+    });
 }
 int synq_sim_engine(const synq_sim* s) { return s && s->impl->persistent() ? 1 : 0; }
 int synq_sim_exact(const synq_sim* s) { return s && s->impl->exact() ? 1 : 0; }
