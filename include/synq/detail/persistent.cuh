@@ -14,18 +14,19 @@
 //   Update(t+1) never leaves the SM and needs no grid barrier.  The neuron
 //   state of the CTA lives in registers for the whole launch.
 // * Frames.  Each CTA compacts its spikes per piece in ascending id order
-//   into the piece's slice of queue slot t % Q and release-stores
-//   {t+1, count} into finfo[slot][piece].  Pieces are numbered in id order,
+//   into the piece's slice of queue slot t % Q and release-stores one word
+//   {t+1, count of its low piece, count of its high piece} into
+//   finfo[slot][cta].  Pieces are numbered in id order,
 //   so concatenating their slices gives the sorted frame.  Receive(t)
 //   consumes frame t-delay+1, finished by every CTA delay-1 steps earlier: the
 //   only cross-CTA wait is an acquire-poll that is normally satisfied at once.
 //   With Q = 2*delay slots no slot is rewritten while a slower CTA may still
 //   read it (a CTA runs at most delay-1 steps ahead of the slowest).
 // * Delivery.  The row segment of spike s inside A_c is
-//   [split[s][c], split[s][c+1]) of the sorted ELL row.  Segments are staged
-//   as 32-target items in shared memory, read with kItemBatch loads in flight
-//   per warp, and counted per (target, source class) with native shared-memory
-//   atomics.  The update re-adds fl(c*w_k) count_k times in ascending class
+//   [split[s][c], split[s][c+1]) of the sorted ELL row.  Segments are cut
+//   into 32-target items, copied global -> shared with cp.async (LDGSTS: no
+//   registers held in flight, one latency round per frame) and counted per
+//   (target, source class) with native shared-memory atomics.  The update re-adds fl(c*w_k) count_k times in ascending class
 //   (= ascending source id) order — exactly the reference's deterministic
 //   float sum, independent of delivery order.
 // * DRAM efficiency.  One step ahead, the full rows of frame due+1 are
@@ -42,12 +43,11 @@
 
 namespace synq::dev {
 
-constexpr int kPersistThreads = 1024;
+constexpr int kPersistThreads = 512;
 constexpr int kMaxTiles = 160;             // CTAs (>= 148 SMs)
 constexpr int kMaxPieces = 2 * kMaxTiles;  // id-ordered pieces
 constexpr int kMaxClasses = 4;
-constexpr uint32_t kItemCap = 2048;  // staged 32-target delivery items per pass (static smem)
-constexpr int kItemBatch = 4;        // row loads in flight per warp
+constexpr int kChunkBatch = 8;  // 16-byte row chunks in flight per lane during delivery
 
 enum prof_slot : int { P_UPDATE = 0, P_PUBLISH, P_POLL, P_GATHER, P_DELIVER, P_STEPS, P_SLOTS = 8 };
 
@@ -62,7 +62,7 @@ struct persist_state {
     const uint32_t* cta_piece;  // [2C]: (A piece, B piece) of every CTA
     uint32_t pitch, n, C, P;
     uint32_t* queue;            // Q slots x n ids
-    unsigned long long* finfo;  // Q x P: (t+1) << 32 | count
+    unsigned long long* finfo;  // Q x C: (t+1) << 32 | first-half piece count << 16 | second-half count
     uint32_t Q;
     int K;
     uint32_t bound[kMaxClasses];
@@ -81,13 +81,17 @@ struct persist_state {
     int64_t log_from;
     uint32_t* flags;
     uint32_t win_cap;          // count-window capacity per class (smem), >= max |A_c|
+    uint32_t a_first;          // 1: the A pieces are pieces 0..C-1 (ids below the B pieces)
+    uint32_t stage_items;      // 32-target items staged in smem per delivery pass
     unsigned long long* prof;  // optional per-CTA phase cycle counters (P_SLOTS each)
 };
 
-// streaming read of adjacency cells: read-only, no L1 allocation
-SYNQ_DEV uint32_t ldg_stream(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+// streaming 16-byte read of adjacency cells: read-only, no L1 allocation
+SYNQ_DEV uint4 ldg_stream4(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
     return v;
 }
 SYNQ_DEV void st_release_gpu(unsigned long long* p, unsigned long long v) {
@@ -149,57 +153,56 @@ SYNQ_DEV uint32_t block_exclusive_scan(uint32_t x, uint32_t* s_tmp, uint32_t& to
     return s_tmp[warp] + incl - x;
 }
 
-// Warp-wide: wait until every piece of frame f is published (or, when
-// nonblocking, only look), acquire, and write the exclusive piece prefix
-// into seg[0..P] (seg[P] = frame size).  Returns false if nonblocking and the
-// frame is not complete yet (seg untouched).
+// Warp-wide: wait until every CTA's slices of frame f are published (or,
+// when nonblocking, only look), acquire, and write the exclusive prefix over
+// the 2C pieces in id order into seg[0..P] (seg[P] = frame size).  Returns
+// false if nonblocking and the frame is not complete yet.
 template <class M>
 SYNQ_DEV bool frame_prefix(const persist_state<M>& ps, int64_t f, uint32_t* seg, bool nonblocking) {
-    const uint32_t lane = threadIdx.x & 31, P = ps.P;
-    const unsigned long long want = static_cast<unsigned long long>(f + 1);
-    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(f % ps.Q) * P;
-    constexpr int kHalf = (kMaxPieces + 63) / 64;  // per lane, in two halves
-    uint32_t cnt[2 * kHalf];
+    const uint32_t lane = threadIdx.x & 31, C = ps.C;
+    const uint32_t want = static_cast<uint32_t>(f + 1);
+    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(f % ps.Q) * C;
+    constexpr int kPer = (kMaxTiles + 31) / 32;
+    unsigned long long val[kPer];
     bool ok = true;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        unsigned long long val[kHalf];
+    for (int q = 0; q < kPer; ++q) {
+        const uint32_t j = q * 32 + lane;
+        val[q] = (j < C) ? ld_relaxed_gpu(fi + j) : (static_cast<unsigned long long>(want) << 32);
+    }
 #pragma unroll
-        for (int q = 0; q < kHalf; ++q) {
-            const uint32_t j = (h * kHalf + q) * 32 + lane;
-            val[q] = (j < P) ? ld_relaxed_gpu(fi + j) : (want << 32);
-        }
-#pragma unroll
-        for (int q = 0; q < kHalf; ++q) {
-            const uint32_t j = (h * kHalf + q) * 32 + lane;
-            if (nonblocking) {
-                ok &= (val[q] >> 32) == want;
-            } else {
-                while ((val[q] >> 32) != want) {
-                    __nanosleep(20);
-                    val[q] = ld_relaxed_gpu(fi + j);
-                }
+    for (int q = 0; q < kPer; ++q) {
+        const uint32_t j = q * 32 + lane;
+        if (nonblocking) {
+            ok &= static_cast<uint32_t>(val[q] >> 32) == want;
+        } else {
+            while (static_cast<uint32_t>(val[q] >> 32) != want) {
+                __nanosleep(20);
+                val[q] = ld_relaxed_gpu(fi + j);
             }
-            cnt[h * kHalf + q] = static_cast<uint32_t>(val[q]);
         }
     }
     if (nonblocking && !__all_sync(0xffffffffu, ok)) return false;
     fence_acq_rel_gpu();  // acquire: the slices are visible to this CTA
+    // first-half pieces (ids low) then second-half pieces, each in CTA order
     uint32_t run = 0;
 #pragma unroll
-    for (int q = 0; q < 2 * kHalf; ++q) {
-        if (q * 32 >= static_cast<int>(P)) break;
-        const uint32_t j = q * 32 + lane;
-        const uint32_t cj = j < P ? cnt[q] : 0;
-        uint32_t incl = cj;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= static_cast<uint32_t>(o)) incl += y;
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            if (q * 32 >= static_cast<int>(C)) break;
+            const uint32_t j = q * 32 + lane;
+            const uint32_t cj = j < C ? static_cast<uint32_t>((val[q] >> (h ? 0 : 16)) & 0xffffu) : 0;
+            uint32_t incl = cj;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= static_cast<uint32_t>(o)) incl += y;
+            }
+            if (j < C) seg[h * C + j] = run + incl - cj;
+            run += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (j < P) seg[j] = run + incl - cj;
-        run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) seg[P] = run;
+    if (lane == 0) seg[2 * C] = run;
     return true;
 }
 
@@ -224,11 +227,13 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     constexpr size_t ACC = population_delivery<M>::acc_field;
     constexpr int NT = kPersistThreads, NW = NT / 32;
 
-    extern __shared__ __align__(16) uint32_t cnt[];       // K x win_cap arrival counters
-    __shared__ uint4 s_item[kItemCap + kItemBatch * NW];  // {row lo, row hi, valid lanes, count offset}
+    extern __shared__ __align__(16) uint32_t cnt[];  // K x win_cap arrival counters | chunk list
+    uint4* chunks = reinterpret_cast<uint4*>(cnt + ((ps.K * ps.win_cap + 31) & ~31u));  // stage_items
     __shared__ uint32_t s_lo[kMaxPieces + 1];
     __shared__ uint32_t s_seg[kMaxPieces + 1];
-    __shared__ uint32_t s_seg2[kMaxPieces + 1];  // frame due+1 (L2 row streaming); [P] = 0 if not ready
+    __shared__ uint32_t s_seg2[kMaxPieces + 1];  // double buffer with s_seg (current / look-ahead frame)
+    __shared__ uint32_t s_ahead;
+    static_assert(NW <= 32, "one scan warp covers every warp");
     __shared__ uint32_t s_wa[NPT * NW], s_wb[NPT * NW];
     __shared__ uint32_t s_tmp[NW + 1];
     __shared__ uint32_t s_mw[NW];
@@ -239,7 +244,6 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     const uint32_t c = blockIdx.x, C = ps.C, P = ps.P;
     for (uint32_t j = tid; j <= P; j += NT) s_lo[j] = ps.piece_lo[j];
     for (uint32_t j = tid; j < ps.K * ps.win_cap; j += NT) cnt[j] = 0;
-    for (uint32_t j = tid; j < kItemBatch * NW; j += NT) s_item[kItemCap + j] = make_uint4(0, 0, 0, 0);
     if (tid < P_SLOTS) s_prof[tid] = 0;
     __syncthreads();
     const uint32_t pa = ps.cta_piece[2 * c], pb = ps.cta_piece[2 * c + 1];
@@ -247,6 +251,9 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     const uint32_t blo = s_lo[pb], nb = s_lo[pb + 1] - blo;  // update-only piece
     unsigned long long my_deliv = 0, my_spikes = 0;
     unsigned long long lc = 0;  // CTA 0: log cursor
+    uint32_t* seg_cur = s_seg;
+    uint32_t* seg_next = s_seg2;
+    bool have_next = false;
     const bool profiling = ps.prof != nullptr && tid == 0;
     long long tp = profiling ? clock64() : 0;
     auto mark = [&](int slot) {
@@ -296,8 +303,16 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                     }
                     detail::pack_get<ACC>::get(v[r]) = acc;
                 }
-                local_neuron<NF> ref{i, &v[r], &rr[r], &live[r], ps.rng};
+                // work on scalar copies: no pointer into the register arrays
+                // escapes, so the state stays in registers (no local memory)
+                values_t<NF> vl = v[r];
+                xorshift rl = rr[r];
+                bool ll = live[r];
+                local_neuron<NF> ref{i, &vl, &rl, &ll, ps.rng};
                 spk[r] = model.update(ref, ps.dt);
+                v[r] = vl;
+                rr[r] = rl;
+                live[r] = ll;
                 mcount += (spk[r] && i >= ps.meas_lo && i < ps.meas_hi) ? 1u : 0u;
             }
             const unsigned ba = __ballot_sync(0xffffffffu, spk[r] && j < na);
@@ -309,12 +324,21 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         }
         for (int o = 16; o; o >>= 1) mcount += __shfl_xor_sync(0xffffffffu, mcount, o);
         if (lane == 0) s_mw[warp] = mcount;
+        if (profiling) {
+            const long long now = clock64();
+            s_prof[6] += now - tp;  // thread 0's own update work
+        }
         __syncthreads();
+        if (profiling) {
+            const long long now = clock64();
+            s_prof[7] += now - tp;  // ... plus waiting for the slowest warp
+        }
         if (warp == 0) {  // exclusive scans of the per-warp counts, ascending local index
             uint32_t runa = 0, runb = 0;
 #pragma unroll
             for (int r = 0; r < NPT; ++r) {
-                const uint32_t xa = s_wa[r * NW + lane], xb = s_wb[r * NW + lane];
+                const uint32_t xa = lane < NW ? s_wa[r * NW + lane] : 0;
+                const uint32_t xb = lane < NW ? s_wb[r * NW + lane] : 0;
                 uint32_t ia = xa, ib = xb;
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o);
@@ -324,12 +348,14 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                         ib += yb;
                     }
                 }
-                s_wa[r * NW + lane] = runa + ia - xa;
-                s_wb[r * NW + lane] = runb + ib - xb;
+                if (lane < NW) {
+                    s_wa[r * NW + lane] = runa + ia - xa;
+                    s_wb[r * NW + lane] = runb + ib - xb;
+                }
                 runa += __shfl_sync(0xffffffffu, ia, 31);
                 runb += __shfl_sync(0xffffffffu, ib, 31);
             }
-            uint32_t mm = s_mw[lane];
+            uint32_t mm = lane < NW ? s_mw[lane] : 0;
             for (int o = 16; o; o >>= 1) mm += __shfl_xor_sync(0xffffffffu, mm, o);
             if (lane == 0) {
                 s_out[0] = runa;
@@ -358,10 +384,9 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         // publish (the release covers the whole CTA's queue writes, ordered
         // before it by the barrier)
         if (tid == 0) {
-            unsigned long long* fi = ps.finfo + static_cast<uint64_t>(slot) * P;
-            const unsigned long long tag = static_cast<unsigned long long>(t + 1) << 32;
-            st_release_gpu(fi + pa, tag | outa);
-            st_release_gpu(fi + pb, tag | outb);
+            const unsigned long long tag = static_cast<unsigned long long>(static_cast<uint32_t>(t + 1)) << 32;
+            const uint32_t first = ps.a_first ? outa : outb, second = ps.a_first ? outb : outa;
+            st_release_gpu(ps.finfo + static_cast<uint64_t>(slot) * C + c, tag | (first << 16) | second);
             if (outa + outb) atomicAdd(&ps.step_spikes[s], outa + outb);
             if (meas) atomicAdd(&ps.step_meas[s], meas);
             my_spikes += outa + outb;
@@ -372,22 +397,29 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         const int64_t due = t - static_cast<int64_t>(ps.delay) + 1;
         if (due < 0) continue;
         const uint32_t* dq = ps.queue + static_cast<uint64_t>(due % ps.Q) * ps.n;
+        // frame due: prefix from the previous step's look-ahead when it was
+        // complete, else poll now; frame due+1: look ahead without waiting
+        uint32_t* seg = have_next ? seg_next : seg_cur;
+        uint32_t* seg_ahead = have_next ? seg_cur : seg_next;
         if (warp == 0) {
-            frame_prefix(ps, due, s_seg, false);
+            if (!have_next) frame_prefix(ps, due, seg, false);
         } else if (warp == 1) {
-            const bool ready = due + 1 < t && frame_prefix(ps, due + 1, s_seg2, true);
-            if (!ready && lane == 0) s_seg2[P] = 0;
+            const bool ready = due + 1 < t && frame_prefix(ps, due + 1, seg_ahead, true);
+            if (lane == 0) s_ahead = ready ? 1u : 0u;
         }
         __syncthreads();
+        have_next = s_ahead != 0;
+        seg_next = seg_ahead;
+        seg_cur = seg;
         mark(P_POLL);
         // stream the FULL rows of frame due+1 into L2 (spike g by CTA g mod C)
-        {
-            const uint32_t S2 = s_seg2[P];
+        if (have_next) {
+            const uint32_t S2 = seg_next[P];
             const uint32_t g2 = c + (NT - 1 - tid) * C;
             if (g2 < S2) {
-                const uint32_t a = piece_of(s_seg2, P, g2);
+                const uint32_t a = piece_of(seg_next, P, g2);
                 const uint32_t* dq2 = ps.queue + static_cast<uint64_t>((due + 1) % ps.Q) * ps.n;
-                const uint32_t src = __ldcg(dq2 + s_lo[a] + (g2 - s_seg2[a]));
+                const uint32_t src = __ldcg(dq2 + s_lo[a] + (g2 - seg_next[a]));
                 const uint32_t deg = __ldg(ps.split + static_cast<uint64_t>(src) * (C + 1) + C);
                 const uint32_t bytes = (deg * 4 + 15) & ~15u;
                 if (bytes)
@@ -397,57 +429,71 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                                  : "memory");
             }
         }
-        const uint32_t S = s_seg[P];
+        const uint32_t S = seg_cur[P];
         const bool logging = ps.log && c == 0 && due >= ps.log_from;
         for (uint32_t c0 = 0; c0 < S; c0 += NT) {
             // one spike per thread: id, this CTA's row segment, item count
             const uint32_t g = c0 + tid;
-            uint32_t len = 0, cofs = 0, nchunk = 0;
+            uint32_t len = 0, cofs = 0, nchunk = 0, beg = 0;
             uint64_t row = 0;
             if (g < S) {
-                const uint32_t a = piece_of(s_seg, P, g);
-                const uint32_t src = __ldcg(dq + s_lo[a] + (g - s_seg[a]));
+                const uint32_t a = piece_of(seg_cur, P, g);
+                const uint32_t src = __ldcg(dq + s_lo[a] + (g - seg_cur[a]));
                 if (logging && lc + g < ps.log_cap) ps.log[lc + g] = src;
                 const uint32_t* sp = ps.split + static_cast<uint64_t>(src) * (C + 1) + c;
                 const uint32_t sb = __ldg(sp), se = __ldg(sp + 1);
                 len = se - sb;
-                row = static_cast<uint64_t>(src) * ps.pitch + sb;
+                row = static_cast<uint64_t>(src) * ps.pitch;  // row start (16-B aligned)
                 cofs = static_cast<uint32_t>(source_class(ps, src)) * ps.win_cap - alo;
-                nchunk = (len + 31) >> 5;
+                // aligned 16-B chunks covering [sb, se)
+                beg = sb;
+                nchunk = len ? (((se + 3) >> 2) - (sb >> 2)) : 0;
                 my_deliv += len;
             }
             uint32_t nitems;
             const uint32_t first = block_exclusive_scan<NT>(nchunk, s_tmp, nitems);
             mark(P_GATHER);
-            // items in passes of kItemCap (a pass is normally the whole frame)
-            for (uint32_t i0 = 0; i0 < nitems; i0 += kItemCap) {
+            // flattened 16-byte chunk list, in passes (a pass is normally the
+            // whole frame): chunk = {row pointer of 4 targets, count offset,
+            // valid word range}; every lane loads its own chunk with a 16-byte
+            // load (consecutive lanes -> consecutive chunks of one segment,
+            // coalesced), kChunkBatch chunks in flight per lane
+            const uint32_t cap = ps.stage_items;
+            for (uint32_t i0 = 0; i0 < nitems; i0 += cap) {
                 for (uint32_t q = 0; q < nchunk; ++q) {
                     const uint32_t it = first + q;
-                    if (it < i0 || it >= i0 + kItemCap) continue;
-                    const uint64_t rq = row + 32ull * q;
-                    s_item[it - i0] = make_uint4(static_cast<uint32_t>(rq), static_cast<uint32_t>(rq >> 32),
-                                                 min(32u, len - 32 * q), cofs);
+                    if (it < i0 || it >= i0 + cap) continue;
+                    const uint32_t w0 = ((beg >> 2) + q) << 2;  // first word of the chunk
+                    const uint32_t lo = beg > w0 ? beg - w0 : 0;
+                    const uint32_t hi = min(4u, beg + len - w0);
+                    const uint64_t a = row + w0;
+                    chunks[it - i0] = make_uint4(static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32), cofs,
+                                                 lo | (hi << 8));
                 }
                 __syncthreads();
-                const uint32_t m = min(kItemCap, nitems - i0);
-                // kItemBatch items per warp in flight: LDS.128 -> LDG -> ATOMS
-                // (items past m read the zero padding: no valid lanes)
-                for (uint32_t it = warp; it < m; it += kItemBatch * NW) {
-                    uint4 d[kItemBatch];
-                    uint32_t tg[kItemBatch];
+                const uint32_t m = min(cap, nitems - i0);
+                for (uint32_t k0 = tid; k0 < m; k0 += kChunkBatch * NT) {
+                    uint4 d[kChunkBatch];
+                    uint4 w[kChunkBatch];
 #pragma unroll
-                    for (int u = 0; u < kItemBatch; ++u) {
-                        const uint32_t k = it + u * NW;
-                        d[u] = s_item[k < m ? k : kItemCap + u * NW + warp];
+                    for (int u = 0; u < kChunkBatch; ++u) {
+                        const uint32_t k = k0 + u * NT;
+                        d[u] = k < m ? chunks[k] : make_uint4(0, 0, 0, 0);
                     }
 #pragma unroll
-                    for (int u = 0; u < kItemBatch; ++u) {
-                        const uint32_t* rp = ps.cells + ((static_cast<uint64_t>(d[u].y) << 32) | d[u].x);
-                        tg[u] = lane < d[u].z ? ldg_stream(rp + lane) : 0xffffffffu;
+                    for (int u = 0; u < kChunkBatch; ++u) {
+                        const uint4* rp = reinterpret_cast<const uint4*>(
+                            ps.cells + ((static_cast<uint64_t>(d[u].y) << 32) | d[u].x));
+                        w[u] = (d[u].w >> 8) ? ldg_stream4(rp) : make_uint4(0, 0, 0, 0);
                     }
 #pragma unroll
-                    for (int u = 0; u < kItemBatch; ++u)
-                        if (tg[u] != 0xffffffffu) atomicAdd(&cnt[d[u].w + tg[u]], 1u);
+                    for (int u = 0; u < kChunkBatch; ++u) {
+                        const uint32_t lo = d[u].w & 0xffu, hi = d[u].w >> 8;
+                        if (lo <= 0 && hi > 0) atomicAdd(&cnt[d[u].z + w[u].x], 1u);
+                        if (lo <= 1 && hi > 1) atomicAdd(&cnt[d[u].z + w[u].y], 1u);
+                        if (lo <= 2 && hi > 2) atomicAdd(&cnt[d[u].z + w[u].z], 1u);
+                        if (hi > 3) atomicAdd(&cnt[d[u].z + w[u].w], 1u);
+                    }
                 }
                 __syncthreads();
             }
@@ -499,9 +545,10 @@ __global__ void k_log_drain(persist_state<M> ps, int64_t from, int64_t to) {
         __syncthreads();
         if (threadIdx.x == 0) {
             uint32_t run = 0;
-            for (uint32_t j = 0; j < P; ++j) {
+            for (uint32_t j = 0; j < P; ++j) {  // piece j: half j / C of CTA j % C's entry
                 s_seg[j] = run;
-                run += static_cast<uint32_t>(ps.finfo[static_cast<uint64_t>(slot) * P + j]);
+                const unsigned long long e = ps.finfo[static_cast<uint64_t>(slot) * ps.C + (j % ps.C)];
+                run += static_cast<uint32_t>((e >> (j < ps.C ? 16 : 0)) & 0xffffu);
             }
             s_seg[P] = run;
         }

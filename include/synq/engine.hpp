@@ -317,6 +317,8 @@ public:
         }
         const double steps = std::max<unsigned long long>(1, h[crit * dev::P_SLOTS + dev::P_STEPS]);
         for (int k = 0; k < 5; ++k) out[5 + k] = h[crit * dev::P_SLOTS + k] / steps;
+        out[10] = h[crit * dev::P_SLOTS + 6] / steps;
+        out[11] = h[crit * dev::P_SLOTS + 7] / steps;
         return out;
     }
 
@@ -482,9 +484,10 @@ private:
         }
         const uint32_t nr = r1 - r0, nu = u1 - u0;
         const uint32_t NTH = dev::kPersistThreads;
+        // ~90% thread occupancy per CTA keeps one neuron per thread (NPT = 1)
         uint32_t C = opt_.tiles ? opt_.tiles
                                 : static_cast<uint32_t>(std::clamp<int64_t>(
-                                      (static_cast<int64_t>(n_) + NTH / 2) / NTH, 1, sms_));
+                                      (static_cast<int64_t>(n_) * 10 + 9 * NTH - 1) / (9 * NTH), 1, sms_));
         C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), n_});
         const uint32_t max_local = 4 * NTH;  // register-resident state: <= 4 neurons per thread
         if (uint64_t(C) * max_local < n_) C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (n_ + max_local - 1) / max_local));
@@ -522,9 +525,13 @@ private:
         int max_smem = 0, dev = 0;
         SYNQ_CUDA(cudaGetDevice(&dev));
         SYNQ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const size_t static_smem = (dev::kItemCap + dev::kItemBatch * 32) * 16 + 3 * (dev::kMaxPieces + 1) * 4 + 8192;
-        const size_t smem = ((size_t(K) * wcap + 3) & ~size_t(3)) * 4;
-        if (smem + static_smem > size_t(max_smem)) return;
+        const size_t static_smem = 3 * (dev::kMaxPieces + 1) * 4 + 8192;
+        const size_t counts = ((size_t(K) * wcap + 31) & ~size_t(31)) * 4;
+        if (counts + static_smem + 1024 * 16 > size_t(max_smem)) return;
+        // the rest of shared memory holds the 16-byte chunk list (16 B per chunk)
+        const size_t chunk_cap = std::min<size_t>(16384, (size_t(max_smem) - static_smem - counts) / 16);
+        const size_t smem = counts + chunk_cap * 16;
+        stage_items_ = static_cast<uint32_t>(chunk_cap);
         npt_select_ = npt_;
         const void* fn = persistent_fn();
         SYNQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -544,7 +551,8 @@ private:
         win_lo_.resize(2 * C);
         win_lo_.upload(cta_piece.data(), 2 * C, stream_);
         build_splits(graph_, alo, split_, stream_);
-        finfo_.resize(size_t(2) * delay_ * P);
+        finfo_.resize(size_t(2) * delay_ * C);
+        a_first_ = u_after ? 1u : 0u;
         K_ = K;
         std::copy(bound, bound + dev::kMaxClasses, bound_);
         std::copy(delta, delta + dev::kMaxClasses, delta_);
@@ -664,6 +672,8 @@ private:
         p.log_from = logged_upto_;
         p.flags = flags_.get();
         p.win_cap = win_cap_;
+        p.a_first = a_first_;
+        p.stage_items = stage_items_;
         p.prof = prof_ ? prof_.get() : nullptr;
         return p;
     }
@@ -916,7 +926,7 @@ private:
     int K_ = 0;
     uint32_t bound_[dev::kMaxClasses] = {};
     float delta_[dev::kMaxClasses] = {};
-    uint32_t win_cap_ = 0, pieces_ = 0;
+    uint32_t win_cap_ = 0, pieces_ = 0, a_first_ = 1, stage_items_ = 0;
     int npt_select_ = 1;
     size_t smem_ = 0;
     int npt_ = 1;

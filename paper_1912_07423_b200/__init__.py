@@ -349,6 +349,7 @@ class Sim:
         names = ["update", "publish", "poll", "gather", "deliver"]
         d = {"mean": dict(zip(names, (round(float(x)) for x in out[:5]))),
              "pacing": dict(zip(names, (round(float(x)) for x in out[5:10]))),
+             "update_detail": {"own_work": round(float(out[10])), "to_first_barrier": round(float(out[11]))},
              "producer": dict(zip(["poll", "ids", "splits", "rebase", "issue"],
                                   (round(float(x)) for x in out[10:15]))), "tiles": tiles.value}
         return d

@@ -17,6 +17,7 @@ print(f"{model} syn={sim.synapses} n={sim.neurons} steps={steps} spikes={c['spik
       f"us/step={ker / steps * 1e6:.2f} launches={sim.kernel_launches()}")
 if prof:
     pc = sim.phase_cycles()
+    print('update detail (pacing):', pc.get('update_detail'))
     for key in ('mean', 'pacing'):
         tot = sum(pc[key].values())
         print(f'phase cycles/step ({key}, {pc["tiles"]} CTAs):', pc[key], 'total', round(tot),
