@@ -18,7 +18,8 @@ reference's `deliveries` (proj/include/synq/engine.hpp:408).
 * cpu_baseline: the UNMODIFIED reference (oracle/_ref/libsynq_ref.so, built
   from /root/reference by oracle/Makefile) on a bounded sample of the same
   network, on this host's cores.
-* --impl reference: the reference's own CPU simulator on all host threads.
+* --impl reference: the reference's own CPU simulator on this host: deterministic
+  (1 thread) and parallel (all threads) modes, the faster reported.
 Inputs are larger than L2 (4.2 GB adjacency vs 126 MB L2), so no L2 flush.
 Under torchrun (N > 1) every rank runs its own 1e9-synapse replica (weak
 scaling); rank 0 prints the JSON line.
@@ -174,31 +175,17 @@ def _ref_deliveries(L, sim) -> int:
     raise RuntimeError("reference stats lack deliveries")
 
 
-def run_reference_arm(args):
-    rank, world, _ = dist_env()
-    if rank != 0:
-        return 0
-    try:
-        import oracle
-
-        if not oracle.have_reference():
-            raise FileNotFoundError("oracle/_ref not built")
-    except Exception as e:
-        print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
-        return 0
-    threads = os.cpu_count() or 1
-    sample = max(100, int(os.environ.get("SYNQ_REF_SAMPLE_STEPS", 500)))
-    import oracle
-
-    ref = oracle.RefLib()
-    L = ref.L
+def _reference_mode(L, args, sample, threads, deterministic):
+    """Build the reference Brunel network and time K samples of `sample`
+    timesteps after W warm-up samples; returns (events, seconds, sim)."""
     opts = L.synq_opts_new()
     L.synq_opts_seed(opts, args.seed)
     L.synq_opts_threads(opts, threads)
+    L.synq_opts_deterministic(opts, 1 if deterministic else 0)
     sim = C.c_void_p()
     if L.synq_sim_new_for_synapses(b"brunel", int(args.synapses), opts, C.byref(sim)) != 0:
-        print(json.dumps({"impl": "reference", "unavailable": L.synq_last_error().decode()}))
-        return 0
+        raise RuntimeError(L.synq_last_error().decode())
+    L.synq_opts_free(opts)
     for _ in range(args.warmup):
         L.synq_sim_run(sim, sample)
     t0 = L.synq_sim_seconds(sim, 3)
@@ -207,7 +194,44 @@ def run_reference_arm(args):
         L.synq_sim_run(sim, sample)
     secs = L.synq_sim_seconds(sim, 3) - t0
     events = _ref_deliveries(L, sim) - d0
-    value = events / secs
+    return events, secs, sim
+
+
+def run_reference_arm(args):
+    """The reference's own CPU simulator on this host: both of its modes on
+    the same Brunel network — deterministic (1 thread, its fastest for this
+    model) and parallel (all host threads) — reporting the faster."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    try:
+        import oracle
+
+        if not oracle.have_reference():
+            raise FileNotFoundError("oracle/_ref not built")
+        ref = oracle.RefLib()
+    except Exception as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
+        return 0
+    L = ref.L
+    threads = os.cpu_count() or 1
+    sample = max(100, int(os.environ.get("SYNQ_REF_SAMPLE_STEPS", 500)))
+    modes = {}
+    info = {}
+    for name, thr, det in (("deterministic", 1, True), ("parallel", threads, False)):
+        try:
+            ev, secs, sim = _reference_mode(L, args, sample, thr, det)
+            modes[name] = (ev / secs, thr, ev, secs)
+            info = {"synapses": int(L.synq_sim_synapses(sim)), "neurons": int(L.synq_sim_neurons(sim))}
+            L.synq_sim_free(sim)
+        except Exception as e:  # reported, the other mode still counts
+            modes[name] = (0.0, thr, 0, 0.0)
+            info.setdefault("errors", []).append(f"{name}: {e}")
+    best = max(modes, key=lambda k: modes[k][0])
+    value, cores, events, secs = modes[best]
+    if value <= 0:
+        print(json.dumps({"impl": "reference", "unavailable": "reference runs failed: %s" % info}))
+        return 0
     bio_per_step = sample / BIO_STEPS
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
@@ -216,16 +240,15 @@ def run_reference_arm(args):
         "wall_s_per_bio_s": secs / (args.steps * bio_per_step),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference builder, seed %d)" % args.seed,
-        "config": {"workload": "brunel", "synapses": int(L.synq_sim_synapses(sim)),
-                   "neurons": int(L.synq_sim_neurons(sim)), "bio_ms_per_step": sample * 0.1,
-                   "mode": f"reference parallel, {threads} threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+        "config": {"workload": "brunel_1e9" if args.synapses == 1e9 else "brunel", **info,
+                   "bio_ms_per_step": sample * 0.1, "mode": f"reference {best}, {cores} thread(s)",
+                   "modes_events_per_s": {k: v[0] for k, v in modes.items()}},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} x {sample} timesteps of Brunel 1e9 after "
-                                   f"{args.warmup} warm-up samples"},
+                                   f"{args.warmup} warm-up samples; faster of deterministic (1 thread) "
+                                   f"and parallel ({threads} threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    L.synq_sim_free(sim)
-    L.synq_opts_free(opts)
     print(json.dumps(line))
     return 0
 
