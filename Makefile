@@ -17,7 +17,15 @@ LIBDIR   := $(PKG)/lib
 OBJDIR   := build/obj
 HDRS     := $(wildcard include/synq/*.hpp include/synq/*.h include/synq/models/*.hpp include/synq/detail/*)
 
-all: lib oracle
+all: lib oracle tests
+
+# C++ model-API tests (device engine with user models), run by tests/test_gpu_cpp.py
+tests: build/test_network
+
+build/test_network: tests/cpp/test_network.cu $(HDRS) $(LIBDIR)/libsynq.so.1
+	@mkdir -p build
+	$(NVCC) -std=c++20 -O2 $(ARCH) -lineinfo -fmad=false --expt-relaxed-constexpr -Iinclude \
+	    -o $@ $< -L$(LIBDIR) -lsynq -Xlinker -rpath,'$$ORIGIN/../$(LIBDIR)'
 
 lib: $(LIBDIR)/libsynq.so.1
 
@@ -42,4 +50,4 @@ oracle:
 clean:
 	rm -rf build $(LIBDIR)
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle tests clean
