@@ -44,7 +44,7 @@
 namespace synq::dev {
 
 constexpr int kPersistThreads = 512;
-constexpr int kMaxTiles = 160;             // CTAs (>= 148 SMs)
+constexpr int kMaxTiles = 160;             // publishers: local CTAs (<= 148 SMs) + remote shards
 constexpr int kMaxPieces = 2 * kMaxTiles;  // id-ordered pieces
 constexpr int kMaxClasses = 4;
 constexpr int kChunkBatch = 8;  // 16-byte row chunks in flight per lane during delivery
@@ -59,10 +59,11 @@ struct persist_state {
     const uint32_t* cells;
     const uint32_t* split;      // [n][C+1]: receive-window boundaries of the CTAs
     const uint32_t* piece_lo;   // [P+1] piece boundaries in id order
-    const uint32_t* cta_piece;  // [2C]: (A piece, B piece) of every CTA
-    uint32_t pitch, n, C, P;
+    const uint32_t* cta_piece;  // [2C]: (A piece, B piece) of every local CTA
+    const uint32_t* piece_src;  // [P]: publisher entry << 1 | half (0: bits 16..31 = A, 1: bits 0..15 = B)
+    uint32_t pitch, n, C, P, E;  // local CTAs, pieces, publishers (C local CTAs + remote shards)
     uint32_t* queue;            // Q slots x n ids
-    unsigned long long* finfo;  // Q x C: (t+1) << 32 | first-half piece count << 16 | second-half count
+    unsigned long long* finfo;  // Q x E frame words, see frame_word()
     uint32_t Q;
     int K;
     uint32_t bound[kMaxClasses];
@@ -81,7 +82,6 @@ struct persist_state {
     int64_t log_from;
     uint32_t* flags;
     uint32_t win_cap;          // count-window capacity per class (smem), >= max |A_c|
-    uint32_t a_first;          // 1: the A pieces are pieces 0..C-1 (ids below the B pieces)
     uint32_t stage_items;      // 32-target items staged in smem per delivery pass
     unsigned long long* prof;  // optional per-CTA phase cycle counters (P_SLOTS each)
 };
@@ -153,30 +153,45 @@ SYNQ_DEV uint32_t block_exclusive_scan(uint32_t x, uint32_t* s_tmp, uint32_t& to
     return s_tmp[warp] + incl - x;
 }
 
-// Warp-wide: wait until every CTA's slices of frame f are published (or,
-// when nonblocking, only look), acquire, and write the exclusive prefix over
-// the 2C pieces in id order into seg[0..P] (seg[P] = frame size).  Returns
-// false if nonblocking and the frame is not complete yet.
+// A published frame word: the 16-bit tag (f+1) (unambiguous because the
+// ring holds Q << 65536 frames) and the publisher's A / B piece spike counts
+// in 24 bits each (a remote shard publishes its whole range as one entry).
+SYNQ_HD unsigned long long frame_word(int64_t f, uint32_t ca, uint32_t cb) {
+    return (static_cast<unsigned long long>(static_cast<uint32_t>(f + 1) & 0xffffu) << 48) |
+           (static_cast<unsigned long long>(ca) << 24) | cb;
+}
+SYNQ_HD uint32_t frame_tag(int64_t f) { return static_cast<uint32_t>(f + 1) & 0xffffu; }
+SYNQ_HD uint32_t word_tag(unsigned long long w) { return static_cast<uint32_t>(w >> 48); }
+SYNQ_HD uint32_t word_a(unsigned long long w) { return static_cast<uint32_t>(w >> 24) & 0xffffffu; }
+SYNQ_HD uint32_t word_b(unsigned long long w) { return static_cast<uint32_t>(w) & 0xffffffu; }
+SYNQ_HD uint32_t word_half(unsigned long long w, uint32_t half) { return half ? word_b(w) : word_a(w); }
+
+// Warp-wide: wait until every publisher (local CTA or remote shard) has
+// published frame f (or, when nonblocking, only look), acquire, and write the
+// exclusive prefix over the P pieces in id order into seg[0..P] (seg[P] =
+// frame size).  fval / psrc: shared scratch (publisher counts) and the piece
+// table.  Returns false if nonblocking and the frame is not complete yet.
 template <class M>
-SYNQ_DEV bool frame_prefix(const persist_state<M>& ps, int64_t f, uint32_t* seg, bool nonblocking) {
-    const uint32_t lane = threadIdx.x & 31, C = ps.C;
-    const uint32_t want = static_cast<uint32_t>(f + 1);
-    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(f % ps.Q) * C;
+SYNQ_DEV bool frame_prefix(const persist_state<M>& ps, int64_t f, uint32_t* seg, unsigned long long* fval,
+                           const uint32_t* psrc, bool nonblocking) {
+    const uint32_t lane = threadIdx.x & 31, E = ps.E, P = ps.P;
+    const uint32_t want = frame_tag(f);
+    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(f % ps.Q) * E;
     constexpr int kPer = (kMaxTiles + 31) / 32;
     unsigned long long val[kPer];
     bool ok = true;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
         const uint32_t j = q * 32 + lane;
-        val[q] = (j < C) ? ld_relaxed_gpu(fi + j) : (static_cast<unsigned long long>(want) << 32);
+        val[q] = (j < E) ? ld_relaxed_gpu(fi + j) : frame_word(f, 0, 0);
     }
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
         const uint32_t j = q * 32 + lane;
         if (nonblocking) {
-            ok &= static_cast<uint32_t>(val[q] >> 32) == want;
+            ok &= word_tag(val[q]) == want;
         } else {
-            while (static_cast<uint32_t>(val[q] >> 32) != want) {
+            while (word_tag(val[q]) != want) {
                 __nanosleep(20);
                 val[q] = ld_relaxed_gpu(fi + j);
             }
@@ -184,25 +199,30 @@ SYNQ_DEV bool frame_prefix(const persist_state<M>& ps, int64_t f, uint32_t* seg,
     }
     if (nonblocking && !__all_sync(0xffffffffu, ok)) return false;
     fence_acq_rel_gpu();  // acquire: the slices are visible to this CTA
-    // first-half pieces (ids low) then second-half pieces, each in CTA order
-    uint32_t run = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            if (q * 32 >= static_cast<int>(C)) break;
-            const uint32_t j = q * 32 + lane;
-            const uint32_t cj = j < C ? static_cast<uint32_t>((val[q] >> (h ? 0 : 16)) & 0xffffu) : 0;
-            uint32_t incl = cj;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= static_cast<uint32_t>(o)) incl += y;
-            }
-            if (j < C) seg[h * C + j] = run + incl - cj;
-            run += __shfl_sync(0xffffffffu, incl, 31);
-        }
+    for (int q = 0; q < kPer; ++q) {
+        const uint32_t j = q * 32 + lane;
+        if (j < E) fval[j] = val[q];
     }
-    if (lane == 0) seg[2 * C] = run;
+    __syncwarp();
+    uint32_t run = 0;
+    for (uint32_t p0 = 0; p0 < P; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        uint32_t cj = 0;
+        if (p < P) {
+            const uint32_t src = psrc[p];
+            cj = word_half(fval[src >> 1], src & 1);
+        }
+        uint32_t incl = cj;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        if (p < P) seg[p] = run + incl - cj;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) seg[P] = run;
+    __syncwarp();
     return true;
 }
 
@@ -232,6 +252,8 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     __shared__ uint32_t s_lo[kMaxPieces + 1];
     __shared__ uint32_t s_seg[kMaxPieces + 1];
     __shared__ uint32_t s_seg2[kMaxPieces + 1];  // double buffer with s_seg (current / look-ahead frame)
+    __shared__ uint32_t s_psrc[kMaxPieces];      // piece table
+    __shared__ unsigned long long s_fval[2][kMaxTiles];  // publisher words (poll / look-ahead scratch)
     __shared__ uint32_t s_ahead;
     static_assert(NW <= 32, "one scan warp covers every warp");
     __shared__ uint32_t s_wa[NPT * NW], s_wb[NPT * NW];
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t c = blockIdx.x, C = ps.C, P = ps.P;
     for (uint32_t j = tid; j <= P; j += NT) s_lo[j] = ps.piece_lo[j];
+    for (uint32_t j = tid; j < P; j += NT) s_psrc[j] = ps.piece_src[j];
     for (uint32_t j = tid; j < ps.K * ps.win_cap; j += NT) cnt[j] = 0;
     if (tid < P_SLOTS) s_prof[tid] = 0;
     __syncthreads();
@@ -384,9 +407,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         // publish (the release covers the whole CTA's queue writes, ordered
         // before it by the barrier)
         if (tid == 0) {
-            const unsigned long long tag = static_cast<unsigned long long>(static_cast<uint32_t>(t + 1)) << 32;
-            const uint32_t first = ps.a_first ? outa : outb, second = ps.a_first ? outb : outa;
-            st_release_gpu(ps.finfo + static_cast<uint64_t>(slot) * C + c, tag | (first << 16) | second);
+            st_release_gpu(ps.finfo + static_cast<uint64_t>(slot) * ps.E + c, frame_word(t, outa, outb));
             if (outa + outb) atomicAdd(&ps.step_spikes[s], outa + outb);
             if (meas) atomicAdd(&ps.step_meas[s], meas);
             my_spikes += outa + outb;
@@ -402,9 +423,9 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         uint32_t* seg = have_next ? seg_next : seg_cur;
         uint32_t* seg_ahead = have_next ? seg_cur : seg_next;
         if (warp == 0) {
-            if (!have_next) frame_prefix(ps, due, seg, false);
+            if (!have_next) frame_prefix(ps, due, seg, s_fval[0], s_psrc, false);
         } else if (warp == 1) {
-            const bool ready = due + 1 < t && frame_prefix(ps, due + 1, seg_ahead, true);
+            const bool ready = due + 1 < t && frame_prefix(ps, due + 1, seg_ahead, s_fval[1], s_psrc, true);
             if (lane == 0) s_ahead = ready ? 1u : 0u;
         }
         __syncthreads();
@@ -420,11 +441,13 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                 const uint32_t a = piece_of(seg_next, P, g2);
                 const uint32_t* dq2 = ps.queue + static_cast<uint64_t>((due + 1) % ps.Q) * ps.n;
                 const uint32_t src = __ldcg(dq2 + s_lo[a] + (g2 - seg_next[a]));
-                const uint32_t deg = __ldg(ps.split + static_cast<uint64_t>(src) * (C + 1) + C);
-                const uint32_t bytes = (deg * 4 + 15) & ~15u;
+                // this shard's receive range of the row: [split[s][0], split[s][C])
+                const uint32_t r0 = __ldg(ps.split + static_cast<uint64_t>(src) * (C + 1)) & ~3u;
+                const uint32_t r1 = __ldg(ps.split + static_cast<uint64_t>(src) * (C + 1) + C);
+                const uint32_t bytes = r1 > r0 ? ((r1 - r0) * 4 + 15) & ~15u : 0;
                 if (bytes)
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                     ps.cells + static_cast<uint64_t>(src) * ps.pitch),
+                                     ps.cells + static_cast<uint64_t>(src) * ps.pitch + r0),
                                  "r"(bytes)
                                  : "memory");
             }
@@ -545,10 +568,11 @@ __global__ void k_log_drain(persist_state<M> ps, int64_t from, int64_t to) {
         __syncthreads();
         if (threadIdx.x == 0) {
             uint32_t run = 0;
-            for (uint32_t j = 0; j < P; ++j) {  // piece j: half j / C of CTA j % C's entry
+            for (uint32_t j = 0; j < P; ++j) {
                 s_seg[j] = run;
-                const unsigned long long e = ps.finfo[static_cast<uint64_t>(slot) * ps.C + (j % ps.C)];
-                run += static_cast<uint32_t>((e >> (j < ps.C ? 16 : 0)) & 0xffffu);
+                const uint32_t src = ps.piece_src[j];
+                const unsigned long long e = ps.finfo[static_cast<uint64_t>(slot) * ps.E + (src >> 1)];
+                run += word_half(e, src & 1);
             }
             s_seg[P] = run;
         }
@@ -565,6 +589,70 @@ __global__ void k_log_drain(persist_state<M> ps, int64_t from, int64_t to) {
     if (threadIdx.x == 0) {
         *ps.log_end = lc;
         if (lc > ps.log_cap) ps.flags[0] = 1;
+    }
+}
+
+// ---- shard exchange: frames produced by this shard's CTAs in
+// steps [t0, t0+b) are packed as
+//   words[0] = b, words[1 + 2k] / [2 + 2k] = A / B spike count of step k,
+//   then the ids of every step: A piece ids (CTA order) then B piece ids.
+// A and B pieces of one shard are contiguous id ranges, so a remote shard's
+// frame slice is two contiguous runs.
+template <class M>
+__global__ void k_export(persist_state<M> ps, int64_t t0, uint32_t b, uint32_t* out) {
+    __shared__ uint32_t s_a[kMaxTiles + 1], s_b[kMaxTiles + 1], s_base;
+    const uint32_t C = ps.C;
+    if (threadIdx.x == 0) {
+        out[0] = b;
+        s_base = 1 + 2 * b;
+    }
+    for (uint32_t k = 0; k < b; ++k) {
+        const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t ra = 0, rb = 0;
+            for (uint32_t c = 0; c < C; ++c) {
+                const unsigned long long e = ps.finfo[static_cast<uint64_t>(slot) * ps.E + c];
+                s_a[c] = ra;
+                s_b[c] = rb;
+                ra += word_a(e);
+                rb += word_b(e);
+            }
+            s_a[C] = ra;
+            s_b[C] = rb;
+            out[1 + 2 * k] = ra;
+            out[2 + 2 * k] = rb;
+        }
+        __syncthreads();
+        const uint32_t base = s_base;
+        const uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
+        for (uint32_t c = 0; c < C; ++c) {
+            const uint32_t alo = ps.piece_lo[ps.cta_piece[2 * c]], blo = ps.piece_lo[ps.cta_piece[2 * c + 1]];
+            for (uint32_t j = threadIdx.x; j < s_a[c + 1] - s_a[c]; j += blockDim.x) out[base + s_a[c] + j] = q[alo + j];
+            for (uint32_t j = threadIdx.x; j < s_b[c + 1] - s_b[c]; j += blockDim.x)
+                out[base + s_a[C] + s_b[c] + j] = q[blo + j];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_base = base + s_a[C] + s_b[C];
+    }
+}
+
+// unpack a remote shard's frames into the ring as publisher `entry`; its
+// pieces start at ids alo / blo
+template <class M>
+__global__ void k_import(persist_state<M> ps, int64_t t0, const uint32_t* in, uint32_t entry, uint32_t alo,
+                         uint32_t blo) {
+    const uint32_t b = in[0];
+    uint32_t base = 1 + 2 * b;
+    for (uint32_t k = 0; k < b; ++k) {
+        const uint32_t ca = in[1 + 2 * k], cb = in[2 + 2 * k];
+        const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
+        uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
+        for (uint32_t j = threadIdx.x; j < ca; j += blockDim.x) q[alo + j] = in[base + j];
+        for (uint32_t j = threadIdx.x; j < cb; j += blockDim.x) q[blo + j] = in[base + ca + j];
+        if (threadIdx.x == 0)
+            ps.finfo[static_cast<uint64_t>(slot) * ps.E + entry] = frame_word(t0 + k, ca, cb);
+        base += ca + cb;
     }
 }
 

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -64,6 +65,10 @@ struct engine_options {
     int persistent = -1;       // -1 auto, 0 never, 1 require (population-delivery models)
     uint32_t tiles = 0;        // persistent CTAs (0 = auto)
     bool profile = false;      // per-phase cycle counters in the persistent kernel
+    // target-partitioned multi-GPU shard: this process owns
+    // shard_rank of shard_world; frames are exchanged with export/import
+    uint32_t shard_rank = 0;
+    uint32_t shard_world = 1;
 };
 
 struct engine_counters {
@@ -191,6 +196,7 @@ public:
         step_spikes_host_.clear();
         expiring_host_.clear();
         logged_upto_ = 0;
+        std::fill(imported_upto_.begin(), imported_upto_.end(), 0);
         const int64_t zero = 0;
         SYNQ_CUDA(cudaMemcpyAsync(t_dev_.get(), &zero, sizeof zero, cudaMemcpyHostToDevice, stream_));
         counters_dev_.zero(stream_);
@@ -233,6 +239,18 @@ public:
 
     void run(int64_t steps) {
         if (steps <= 0) return;
+        if (sharded()) {
+            // a shard may only run steps whose due frames are all present:
+            // at most delay-1 steps past the frames imported from every rank
+            if (steps > int64_t(delay_) - 1)
+                throw std::invalid_argument("sharded run: at most delay-1 steps between frame exchanges");
+            for (uint32_t q = 0; q < opt_.shard_world; ++q)
+                if (q != opt_.shard_rank && imported_upto_[q] < t_ + steps - int64_t(delay_) + 1)
+                    throw std::logic_error("sharded run: frames of rank " + std::to_string(q) +
+                                           " not imported (export/import after every run)");
+            last_batch_t0_ = t_;
+            last_batch_b_ = static_cast<uint32_t>(steps);
+        }
         push_mirrors();
         auto t0 = clock::now();
         SYNQ_CUDA(cudaEventRecord(ev_[0], stream_));
@@ -241,7 +259,7 @@ public:
             run_batch(static_cast<uint32_t>(b));
             steps -= b;
         }
-        if (persistent_ && log_ids_ && logged_upto_ < t_) drain_log();
+        if (persistent_ && log_ids_ && logged_upto_ < t_ && !sharded()) drain_log();
         SYNQ_CUDA(cudaEventRecord(ev_[1], stream_));
         SYNQ_CUDA(cudaEventSynchronize(ev_[1]));
         float ms = 0;
@@ -294,6 +312,65 @@ public:
     uint64_t h2d_bytes() const { return h2d_bytes_; }
     uint64_t d2h_bytes() const { return d2h_bytes_; }
     unsigned tiles() const { return tiles_; }
+
+    // ---- multi-GPU shard exchange -------------------------
+    bool sharded() const { return opt_.shard_world > 1; }
+    // words needed to export the frames of the last run() (upper bound)
+    uint64_t export_capacity() const {
+        return 1 + 2ull * (delay_ ? delay_ : 1) + uint64_t(delay_) * ((shard_lo_[1] - shard_lo_[0]) + (shard_lo_[3] - shard_lo_[2]));
+    }
+    // pack this shard's frames of the last run() into dst (device or host
+    // memory); returns the words written
+    uint64_t export_frames(void* dst, uint64_t cap_words, bool device_dst) {
+        if constexpr (population_model) {
+            if (!sharded() || !persistent_) throw std::logic_error("export_frames: not a persistent shard");
+            const uint64_t need = export_capacity();
+            if (xbuf_.size() < need) xbuf_.resize(need);
+            dev::k_export<Model><<<1, 1024, 0, stream_>>>(pstate(), last_batch_t0_, last_batch_b_, xbuf_.get());
+            SYNQ_CUDA(cudaGetLastError());
+            uint64_t words = 1 + 2ull * last_batch_b_;
+            std::vector<uint32_t> counts(2 * size_t(last_batch_b_));
+            if (!counts.empty())
+                SYNQ_CUDA(cudaMemcpyAsync(counts.data(), xbuf_.get() + 1, counts.size() * 4, cudaMemcpyDeviceToHost, stream_));
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            for (uint32_t v : counts) words += v;
+            if (words > cap_words) throw std::invalid_argument("export_frames: destination too small");
+            SYNQ_CUDA(cudaMemcpyAsync(dst, xbuf_.get(), words * 4,
+                                      device_dst ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream_));
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            return words;
+        } else {
+            throw std::logic_error("export_frames: model has no persistent engine");
+        }
+    }
+    // unpack rank `from`'s exported frames (batch starting at the same step
+    // as this shard's last run)
+    void import_frames(const void* src, uint64_t words, uint32_t from, bool device_src) {
+        if constexpr (population_model) {
+            if (!sharded() || !persistent_) throw std::logic_error("import_frames: not a persistent shard");
+            if (from >= opt_.shard_world || from == opt_.shard_rank) throw std::invalid_argument("import_frames: bad rank");
+            if (xbuf_.size() < words) xbuf_.resize(words);
+            SYNQ_CUDA(cudaMemcpyAsync(xbuf_.get(), src, words * 4,
+                                      device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
+            uint32_t b = 0;
+            SYNQ_CUDA(cudaMemcpyAsync(&b, xbuf_.get(), 4, cudaMemcpyDeviceToHost, stream_));
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            const int64_t t0 = imported_upto_[from];
+            dev::k_import<Model><<<1, 1024, 0, stream_>>>(pstate(), t0, xbuf_.get(), remote_[from][0],
+                                                         remote_[from][1], remote_[from][2]);
+            SYNQ_CUDA(cudaGetLastError());
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            imported_upto_[from] = t0 + b;
+        } else {
+            throw std::logic_error("import_frames: model has no persistent engine");
+        }
+    }
+    // this shard's receiving [lo, hi) and update-only [lo, hi) neuron ids
+    std::array<uint32_t, 4> shard_range() const {
+        return sharded() ? shard_lo_ : std::array<uint32_t, 4>{0, n_, n_, n_};
+    }
+    uint32_t shard_rank() const { return opt_.shard_rank; }
+    uint32_t shard_world() const { return opt_.shard_world; }
     // persistent-kernel phase profile: average cycles per step per CTA for
     // update, publish, poll, gather, deliver (opt.profile only)
     std::vector<double> phase_cycles() const {
@@ -323,6 +400,7 @@ public:
     }
 
     void set_spike_tap(tap_fn fn) {
+        if (fn && sharded()) throw std::invalid_argument("spike taps are not available on a shard");
         tap_ = std::move(fn);
         if (tap_) {
             ensure_log();
@@ -438,6 +516,10 @@ private:
             if (opt_.persistent == 1 && !persistent_)
                 throw std::invalid_argument("persistent engine requested but the network does not fit it");
         }
+        if (sharded() && !persistent_)
+            throw std::invalid_argument("sharding needs the persistent engine (population-delivery model)");
+        if (sharded() && delay_ < 2)
+            throw std::invalid_argument("sharding needs a delay of at least 2 steps (frames are exchanged every delay-1 steps)");
         Q_ = persistent_ ? 2 * delay_ : delay_;
         queue_.resize(std::max<size_t>(1, size_t(Q_) * n_));
         qcount_.resize(Q_);
@@ -482,7 +564,7 @@ private:
             u1 = r0;
             u_after = false;
         }
-        const uint32_t nr = r1 - r0, nu = u1 - u0;
+        const uint32_t nr = r1 - r0;
         const uint32_t NTH = dev::kPersistThreads;
         // ~90% thread occupancy per CTA keeps one neuron per thread (NPT = 1)
         uint32_t C = opt_.tiles ? opt_.tiles
@@ -491,18 +573,40 @@ private:
         C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), n_});
         const uint32_t max_local = 4 * NTH;  // register-resident state: <= 4 neurons per thread
         if (uint64_t(C) * max_local < n_) C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (n_ + max_local - 1) / max_local));
-        // A pieces by receive cost (update share + expected arrivals), B by count
+        // shards: contiguous rank ranges of the receiving region (by receive
+        // cost) and of the update-only region (by count); then this rank's
+        // range into C local pieces of each kind
+        const uint32_t W = std::max<uint32_t>(1, opt_.shard_world), R = opt_.shard_rank;
+        if (R >= W) throw std::invalid_argument("shard rank out of range");
         std::vector<double> prefix(size_t(nr) + 1, 0.0);
         for (uint32_t k = 0; k < nr; ++k) prefix[k + 1] = prefix[k] + 16.0 + 0.003 * indeg[r0 + k];
-        std::vector<uint32_t> alo(C + 1), blo(C + 1);
-        for (uint32_t c = 0; c <= C; ++c) {
-            const double target = prefix[nr] * c / C;
-            alo[c] = r0 + static_cast<uint32_t>(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
-            blo[c] = u0 + static_cast<uint32_t>(uint64_t(nu) * c / C);
+        auto cut_cost = [&](uint32_t lo, uint32_t hi, uint32_t parts) {  // ids in [lo, hi) of the region
+            std::vector<uint32_t> b(parts + 1);
+            const double c0 = prefix[lo - r0], c1 = prefix[hi - r0];
+            for (uint32_t c = 0; c <= parts; ++c) {
+                const double target = c0 + (c1 - c0) * c / parts;
+                b[c] = r0 + static_cast<uint32_t>(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
+                b[c] = std::clamp(b[c], lo, hi);
+            }
+            b[0] = lo;
+            b[parts] = hi;
+            for (uint32_t c = 1; c <= parts; ++c) b[c] = std::max(b[c], b[c - 1]);
+            return b;
+        };
+        auto cut_count = [](uint32_t lo, uint32_t hi, uint32_t parts) {
+            std::vector<uint32_t> b(parts + 1);
+            for (uint32_t c = 0; c <= parts; ++c) b[c] = lo + static_cast<uint32_t>(uint64_t(hi - lo) * c / parts);
+            return b;
+        };
+        const std::vector<uint32_t> ra = cut_cost(r0, r1, W), ub = cut_count(u0, u1, W);
+        if (W > 1) {  // the local shard sizes its CTA count by its own neurons
+            const uint64_t mine = (ra[R + 1] - ra[R]) + (ub[R + 1] - ub[R]);
+            if (!opt_.tiles)
+                C = static_cast<uint32_t>(std::clamp<int64_t>((static_cast<int64_t>(mine) * 10 + 9 * NTH - 1) / (9 * NTH), 1, sms_));
         }
-        alo[0] = r0;
-        alo[C] = r1;
-        for (uint32_t c = 1; c <= C; ++c) alo[c] = std::max(alo[c], alo[c - 1]);
+        if (C + W - 1 > uint32_t(dev::kMaxTiles)) return;
+        if (2ull * delay_ >= (1u << 15)) return;  // 16-bit frame tags need Q << 65536
+        const std::vector<uint32_t> alo = cut_cost(ra[R], ra[R + 1], C), blo = cut_count(ub[R], ub[R + 1], C);
         uint32_t longest = 0, wcap = 1;
         for (uint32_t c = 0; c < C; ++c) {
             longest = std::max(longest, (alo[c + 1] - alo[c]) + (blo[c + 1] - blo[c]));
@@ -510,17 +614,38 @@ private:
         }
         if (longest > max_local) return;  // cannot hold the state: per-step kernel graph
         npt_ = longest <= NTH ? 1 : (longest <= 2 * NTH ? 2 : 4);
-        // pieces in id order
-        const uint32_t P = 2 * C;
-        std::vector<uint32_t> piece_lo(P + 1), cta_piece(2 * C);
-        for (uint32_t c = 0; c < C; ++c) {
-            const uint32_t ia = u_after ? c : C + c, ib = u_after ? C + c : c;
-            piece_lo[ia] = alo[c];
-            piece_lo[ib] = blo[c];
-            cta_piece[2 * c] = ia;
-            cta_piece[2 * c + 1] = ib;
+        // pieces in id order; publishers: local CTAs 0..C-1, then remote shards
+        const uint32_t E = C + W - 1;
+        auto remote_entry = [&](uint32_t q) { return C + (q < R ? q : q - 1); };
+        std::vector<uint32_t> piece_lo, piece_src, cta_piece(2 * C);
+        remote_.assign(W, {0, 0, 0});
+        auto emit_region = [&](int half) {
+            for (uint32_t q = 0; q < W; ++q) {
+                if (q == R) {
+                    for (uint32_t c = 0; c < C; ++c) {
+                        cta_piece[2 * c + half] = static_cast<uint32_t>(piece_lo.size());
+                        piece_lo.push_back(half ? blo[c] : alo[c]);
+                        piece_src.push_back((c << 1) | half);
+                    }
+                } else {
+                    piece_lo.push_back(half ? ub[q] : ra[q]);
+                    piece_src.push_back((remote_entry(q) << 1) | half);
+                    remote_[q][0] = remote_entry(q);
+                    remote_[q][1 + half] = half ? ub[q] : ra[q];
+                }
+            }
+        };
+        if (u_after) {
+            emit_region(0);
+            emit_region(1);
+        } else {
+            emit_region(1);
+            emit_region(0);
         }
-        piece_lo[P] = n_;
+        const uint32_t P = static_cast<uint32_t>(piece_lo.size());
+        piece_lo.push_back(n_);
+        for (uint32_t p = 0; p + 1 < piece_lo.size(); ++p)  // pieces must tile the id space in order
+            if (piece_lo[p] > piece_lo[p + 1]) throw device_error("internal: shard pieces out of order");
         // dynamic smem: counts only (delivery items are static)
         int max_smem = 0, dev = 0;
         SYNQ_CUDA(cudaGetDevice(&dev));
@@ -545,14 +670,18 @@ private:
 
         tiles_ = C;
         pieces_ = P;
+        publishers_ = E;
         tile_lo_host_ = piece_lo;
         tile_lo_.resize(P + 1);
         tile_lo_.upload(piece_lo.data(), P + 1, stream_);
         win_lo_.resize(2 * C);
         win_lo_.upload(cta_piece.data(), 2 * C, stream_);
+        piece_src_.resize(P);
+        piece_src_.upload(piece_src.data(), P, stream_);
         build_splits(graph_, alo, split_, stream_);
-        finfo_.resize(size_t(2) * delay_ * C);
-        a_first_ = u_after ? 1u : 0u;
+        finfo_.resize(size_t(2) * delay_ * E);
+        shard_lo_ = {ra[R], ra[R + 1], ub[R], ub[R + 1]};
+        imported_upto_.assign(W, 0);
         K_ = K;
         std::copy(bound, bound + dev::kMaxClasses, bound_);
         std::copy(delta, delta + dev::kMaxClasses, delta_);
@@ -649,10 +778,12 @@ private:
         p.split = split_.get();
         p.piece_lo = tile_lo_.get();
         p.cta_piece = win_lo_.get();
+        p.piece_src = piece_src_.get();
         p.pitch = graph_.pitch;
         p.n = n_;
         p.C = tiles_;
         p.P = pieces_;
+        p.E = publishers_;
         p.queue = queue_.get();
         p.finfo = finfo_.get();
         p.Q = Q_;
@@ -672,7 +803,6 @@ private:
         p.log_from = logged_upto_;
         p.flags = flags_.get();
         p.win_cap = win_cap_;
-        p.a_first = a_first_;
         p.stage_items = stage_items_;
         p.prof = prof_ ? prof_.get() : nullptr;
         return p;
@@ -926,7 +1056,15 @@ private:
     int K_ = 0;
     uint32_t bound_[dev::kMaxClasses] = {};
     float delta_[dev::kMaxClasses] = {};
-    uint32_t win_cap_ = 0, pieces_ = 0, a_first_ = 1, stage_items_ = 0;
+    uint32_t win_cap_ = 0, pieces_ = 0, publishers_ = 0, stage_items_ = 0;
+    dev_array<uint32_t> piece_src_;
+    // shard exchange
+    std::vector<std::array<uint32_t, 3>> remote_;  // per rank: publisher entry, A lo, B lo
+    std::array<uint32_t, 4> shard_lo_{};           // this shard: A [lo, hi), B [lo, hi)
+    std::vector<int64_t> imported_upto_;            // frames < this imported, per rank
+    dev_array<uint32_t> xbuf_;                      // export / import staging
+    int64_t last_batch_t0_ = 0;
+    uint32_t last_batch_b_ = 0;
     int npt_select_ = 1;
     size_t smem_ = 0;
     int npt_ = 1;

@@ -130,6 +130,11 @@ def lib() -> C.CDLL:
     sig("synq_sim_transfer_bytes", st, vp, vp)
     sig("synq_sim_set_record", st, vp, C.c_int)
     sig("synq_opts_profile", st, vp, C.c_int)
+    sig("synq_opts_shard", st, vp, u32, u32)
+    sig("synq_sim_shard_capacity", u64, vp)
+    sig("synq_sim_shard_range", st, vp, C.POINTER(u32))
+    sig("synq_sim_shard_export", st, vp, vp, u64, C.c_int, C.POINTER(u64))
+    sig("synq_sim_shard_import", st, vp, vp, u64, u32, C.c_int)
     sig("synq_sim_phase_cycles", st, vp, vp, C.POINTER(u32))
     _lib = L
     return L
@@ -149,7 +154,7 @@ class Opts:
 
     def __init__(self, seed=None, threads=None, deterministic=None, dt=None, delay=None,
                  record=None, defaults_file=None, params=None, batch_steps=None,
-                 persistent=None, tiles=None, profile=None):
+                 persistent=None, tiles=None, profile=None, shard=None):
         self.h = lib().synq_opts_new()
         if not self.h:
             raise MemoryError("synq_opts_new")
@@ -178,6 +183,8 @@ class Opts:
             check(L.synq_opts_tiles(self.h, tiles))
         if profile is not None:
             check(L.synq_opts_profile(self.h, int(profile)))
+        if shard is not None:
+            check(L.synq_opts_shard(self.h, int(shard[0]), int(shard[1])))
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -353,6 +360,36 @@ class Sim:
              "producer": dict(zip(["poll", "ids", "splits", "rebase", "issue"],
                                   (round(float(x)) for x in out[10:15]))), "tiles": tiles.value}
         return d
+
+    # ---- multi-GPU shard exchange
+    def shard_range(self):
+        """((receiving lo, hi), (update-only lo, hi)) neuron ids of this shard."""
+        out = (C.c_uint32 * 4)()
+        check(lib().synq_sim_shard_range(self.h, out))
+        return (out[0], out[1]), (out[2], out[3])
+
+    def shard_capacity(self) -> int:
+        return int(lib().synq_sim_shard_capacity(self.h))
+
+    def shard_export(self, buf=None, device_ptr: int | None = None, capacity: int | None = None):
+        """Pack the last run's frames.  With device_ptr the words go to device
+        memory (e.g. a torch tensor's data_ptr()); otherwise into a numpy
+        array (returned)."""
+        words = C.c_uint64()
+        if device_ptr is not None:
+            check(lib().synq_sim_shard_export(self.h, C.c_void_p(device_ptr), capacity, 1, C.byref(words)))
+            return int(words.value)
+        cap = self.shard_capacity()
+        out = np.empty(max(cap, 1), np.uint32)
+        check(lib().synq_sim_shard_export(self.h, _p(out), cap, 0, C.byref(words)))
+        return out[: words.value].copy()
+
+    def shard_import(self, words, from_rank: int, device_ptr: int | None = None, nwords: int | None = None):
+        if device_ptr is not None:
+            check(lib().synq_sim_shard_import(self.h, C.c_void_p(device_ptr), nwords, from_rank, 1))
+        else:
+            w = np.ascontiguousarray(words, np.uint32)
+            check(lib().synq_sim_shard_import(self.h, _p(w), len(w), from_rank, 0))
 
     def set_record(self, on: bool):
         check(lib().synq_sim_set_record(self.h, int(on)))

@@ -6,6 +6,7 @@
 // Differences are confined to where the work runs: every simulation here is a
 // synq::network<M> on the B200 (include/synq/engine.hpp).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -71,6 +72,10 @@ public:
     virtual void set_record(bool on) = 0;
     virtual std::vector<double> phase_cycles() const = 0;
     virtual unsigned tiles() const = 0;
+    virtual uint64_t shard_capacity() const = 0;
+    virtual std::array<uint32_t, 4> shard_range() const = 0;
+    virtual uint64_t shard_export(void* dst, uint64_t cap, bool device) = 0;
+    virtual void shard_import(const void* src, uint64_t words, uint32_t from, bool device) = 0;
 
     void write_stats(std::ostream& out) const;
     void write_stats_to(const std::string& path) const;
@@ -128,6 +133,14 @@ public:
 
     std::vector<double> phase_cycles() const override { return net_->phase_cycles(); }
     unsigned tiles() const override { return net_->tiles(); }
+    std::array<uint32_t, 4> shard_range() const override { return net_->shard_range(); }
+    uint64_t shard_capacity() const override { return net_->sharded() ? net_->export_capacity() : 0; }
+    uint64_t shard_export(void* dst, uint64_t cap, bool device) override {
+        return net_->export_frames(dst, cap, device);
+    }
+    void shard_import(const void* src, uint64_t words, uint32_t from, bool device) override {
+        net_->import_frames(src, words, from, device);
+    }
     void set_record(bool on) override {
         record_ = on;
         raster_.records.clear();
@@ -638,6 +651,41 @@ synq_status synq_opts_tiles(synq_opts* o, uint32_t tiles) {
     SYNQ_CHECK_HANDLE(o);
     o->cfg.engine.tiles = tiles;
     return SYNQ_OK;
+}
+synq_status synq_opts_shard(synq_opts* o, uint32_t rank, uint32_t world) {
+    SYNQ_CHECK_HANDLE(o);
+    if (world < 1 || rank >= world) {
+        set_error("shard: need rank < world, world >= 1");
+        return SYNQ_ERR_INVALID_ARGUMENT;
+    }
+    o->cfg.engine.shard_rank = rank;
+    o->cfg.engine.shard_world = world;
+    return SYNQ_OK;
+}
+synq_status synq_sim_shard_range(const synq_sim* s, uint32_t out[4]) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(out);
+    const auto r = s->impl->shard_range();
+    std::copy(r.begin(), r.end(), out);
+    return SYNQ_OK;
+}
+uint64_t synq_sim_shard_capacity(const synq_sim* s) { return s ? s->impl->shard_capacity() : 0; }
+synq_status synq_sim_shard_export(synq_sim* s, void* dst, uint64_t capacity, int device, uint64_t* words) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(dst);
+    SYNQ_CHECK_HANDLE(words);
+    return guarded([&] {
+        *words = s->impl->shard_export(dst, capacity, device != 0);
+        return SYNQ_OK;
+    });
+}
+synq_status synq_sim_shard_import(synq_sim* s, const void* src, uint64_t words, uint32_t from_rank, int device) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(src);
+    return guarded([&] {
+        s->impl->shard_import(src, words, from_rank, device != 0);
+        return SYNQ_OK;
+    });
 }
 synq_status synq_opts_profile(synq_opts* o, int on) {
     SYNQ_CHECK_HANDLE(o);

@@ -213,22 +213,19 @@ __global__ void k_splits(const uint32_t* __restrict__ cells, const uint32_t* __r
         const uint64_t s = x / (tiles + 1);
         const uint32_t c = static_cast<uint32_t>(x % (tiles + 1));
         const uint32_t d = degree[s];
-        uint32_t pos;
-        if (c == tiles) {
-            pos = d;
-        } else {
-            const uint32_t key = tile_lo[c];
-            const uint32_t* row = cells + s * pitch;
-            uint32_t lo = 0, hi = d;  // lower_bound
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (row[mid] < key)
-                    lo = mid + 1;
-                else
-                    hi = mid;
-            }
-            pos = lo;
+        // lower_bound of the boundary; the last boundary of a shard is not
+        // the end of the row (its targets stop at the shard's range)
+        const uint32_t key = tile_lo[c];
+        const uint32_t* row = cells + s * pitch;
+        uint32_t lo = 0, hi = d;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (row[mid] < key)
+                lo = mid + 1;
+            else
+                hi = mid;
         }
+        const uint32_t pos = lo;
         split[x] = pos;
     }
 }
