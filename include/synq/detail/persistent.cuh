@@ -49,7 +49,10 @@ constexpr int kMaxPieces = 2 * kMaxTiles;  // id-ordered pieces
 constexpr int kMaxClasses = 4;
 constexpr int kChunkBatch = 8;  // 16-byte row chunks in flight per lane during delivery
 
-enum prof_slot : int { P_UPDATE = 0, P_PUBLISH, P_POLL, P_GATHER, P_DELIVER, P_STEPS, P_SLOTS = 8 };
+enum prof_slot : int { P_UPDATE = 0, P_PUBLISH, P_POLL, P_GATHER, P_DELIVER, P_STEPS, P_SLOTS = 16 };
+// pipelined kernel only: 6 delivery wait for frames, 7 delivery passes,
+// 8 update first barrier, 9 update scan, 10 delivery frame prefixes,
+// 11 delivery chunk list
 
 template <class M>
 struct persist_state {
@@ -84,6 +87,11 @@ struct persist_state {
     uint32_t win_cap;          // count-window capacity per class (smem), >= max |A_c|
     uint32_t stage_items;      // 32-target items staged in smem per delivery pass
     unsigned long long* prof;  // optional per-CTA phase cycle counters (P_SLOTS each)
+    // pipelined engine (pipeline.cuh)
+    uint32_t R;       // count-ring slots (frames in flight between delivery and update)
+    uint32_t lead;    // update runs at most this many frames ahead of local delivery
+    uint32_t pf_cap;  // row-prefetch windows held in smem (0: no L2 row prefetch)
+    uint32_t lag;     // frame f is delivered once frame f + lag is complete (its rows are in L2)
 };
 
 // streaming 16-byte read of adjacency cells: read-only, no L1 allocation
@@ -224,6 +232,23 @@ SYNQ_DEV bool frame_prefix(const persist_state<M>& ps, int64_t f, uint32_t* seg,
     if (lane == 0) seg[P] = run;
     __syncwarp();
     return true;
+}
+
+// Warp-wide: is frame f published by every publisher (blocking: wait)?
+template <class M>
+SYNQ_DEV bool frame_complete(const persist_state<M>& ps, int64_t f, bool blocking) {
+    const uint32_t lane = threadIdx.x & 31, E = ps.E;
+    const uint32_t want = frame_tag(f);
+    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(f % ps.Q) * E;
+    bool ok = true;
+    for (uint32_t j = lane; j < E; j += 32) {
+        if (blocking) {
+            while (word_tag(ld_relaxed_gpu(fi + j)) != want) __nanosleep(20);
+        } else {
+            ok &= word_tag(ld_relaxed_gpu(fi + j)) == want;
+        }
+    }
+    return __all_sync(0xffffffffu, ok);
 }
 
 // the piece holding frame position g: last j with seg[j] <= g

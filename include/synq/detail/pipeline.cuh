@@ -1,0 +1,477 @@
+#pragma once
+// Pipelined persistent engine for population-delivery models (vogels /
+// brunel; trait synq::population_delivery<M>): the default step kernel.
+//
+// Reference semantics are those of k_persistent (persistent.cuh):
+// engine.hpp:188-218 (step), 308-341 (update), 369-409 (receive),
+// lif.hpp:23-49.  Ownership (pieces A_c / B_c), frames (per-piece slices of
+// queue slot f % Q + one release-stored word per publisher) and exactness
+// (arrivals counted per (target, source class), re-added in class order by
+// the update) are the same.  What changes is the schedule.
+//
+// Receive(t) consumes frame t-delay+1, and its arrivals are first read by
+// Update(t+1).  A frame is therefore needed delay steps after it was
+// published, and the delivery work of a step is NOT on the update's critical
+// path.  k_persistent still runs update -> publish -> poll -> gather ->
+// deliver as one serial chain per step (a chain of L2/HBM round trips,
+// ~15 us per step at Brunel 1e9).  Here every CTA is warp-specialised:
+//
+// * Update warps (UW warps, neuron state in registers) run Update(t):
+//   fold the arrival counts of frame t-delay from the count ring, call
+//   model.update, compact the spikes per piece, publish the frame, and
+//   stream the full rows of their spikes into L2
+//   (cp.async.bulk.prefetch.L2) for the deliverers of every CTA.
+// * Delivery warps stream frames into a ring of R per-frame count windows
+//   in shared memory (slot = frame mod R).  Each pass takes EVERY frame that
+//   is complete (up to kPipeMaxBatch): the more the deliverers lag, the
+//   larger their batches, so latency is amortised over more work.  A
+//   delivery pass is: poll (one warp per frame), gather (spike ids, row
+//   windows, 16-byte chunk list), then 16-byte row-chunk loads with
+//   shared-memory counting atomics (ATOMS.POPC.INC).
+//
+// Flow control (all shared-memory release/acquire inside the CTA):
+// * frame f is delivered once frame f + lag is complete: its publishers
+//   streamed its rows into L2 meanwhile, so HBM sees whole-row bulk reads
+//   and the deliverers' 16-byte chunk loads hit L2;
+// * update(t) waits until frame t - min(lead, delay) is delivered locally.
+//   This is needed for t - delay.  The lead bounds how far the update can
+//   run ahead, so the rows it prefetched are still in L2 when they are
+//   delivered;
+// * delivering frame f into slot f mod R waits until update(f - R + delay)
+//   folded (and zeroed) that slot's previous frame;
+// * the queue ring (Q = 2*delay slots) is never overwritten before every CTA
+//   delivered the frame: a CTA at update(t) implies every CTA delivered
+//   frame >= t - 2*lead >= t - Q.
+// Frames are indexed relative to the launch: rel(f) = f - (t0 - delay), so a
+// launch of nsteps delivers rel 1 .. nsteps and update step s folds rel s.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "synq/detail/persistent.cuh"
+
+namespace synq::dev {
+
+constexpr int kPipeThreads = 512;
+constexpr int kPipeMaxBatch = 8;  // frames per delivery pass
+
+SYNQ_DEV uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+SYNQ_DEV void st_release_cta(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+SYNQ_DEV uint32_t ld_acquire_cta(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+SYNQ_DEV void named_bar(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+// wait until *p >= want (every calling thread acquires)
+SYNQ_DEV void wait_at_least(const uint32_t* p, uint32_t want) {
+    while (ld_acquire_cta(p) < want) __nanosleep(32);
+}
+
+// exclusive scan of one value per thread over a named-barrier group of NTH
+// threads starting at warp W0
+template <int NTH, int W0, int BAR>
+SYNQ_DEV uint32_t group_exclusive_scan(uint32_t x, uint32_t* s_tmp, uint32_t& total) {
+    constexpr int NWG = NTH / 32;
+    const uint32_t lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - W0;
+    uint32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += y;
+    }
+    if (lane == 31) s_tmp[warp] = incl;
+    named_bar(BAR, NTH);
+    if (warp == 0) {
+        const uint32_t w = lane < NWG ? s_tmp[lane] : 0;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= static_cast<uint32_t>(o)) wi += y;
+        }
+        if (lane < NWG) s_tmp[lane] = wi - w;
+        if (lane == 31) s_tmp[NWG] = wi;
+    }
+    named_bar(BAR, NTH);
+    total = s_tmp[NWG];
+    const uint32_t r = s_tmp[warp] + incl - x;
+    named_bar(BAR, NTH);  // s_tmp may be reused right after
+    return r;
+}
+
+// UW update warps (NPT neurons per update thread); the other warps deliver
+template <class M, int UW, int NPT>
+__global__ void __launch_bounds__(kPipeThreads, 1)
+    k_pipeline(M model, persist_state<M> ps, int64_t t0, int32_t nsteps) {
+    using NF = typename M::neuron_fields;
+    constexpr size_t ACC = population_delivery<M>::acc_field;
+    constexpr int NT = kPipeThreads, NW = NT / 32;
+    constexpr int UT = UW * 32, DT = NT - UT, DW = NW - UW;
+    constexpr uint32_t BAR_U = 1, BAR_D = 2;
+    static_assert(DW >= kPipeMaxBatch, "one polling warp per frame of a pass");
+
+    // dynamic: count ring (R x K x win_cap) | row prefetch windows (pf) | chunk list
+    extern __shared__ __align__(16) uint32_t ring[];
+    const uint32_t ring_words = (ps.R * ps.K * ps.win_cap + 3) & ~3u;
+    uint2* pf = reinterpret_cast<uint2*>(ring + ring_words);
+    uint2* chunks = pf + ps.pf_cap;
+    __shared__ uint32_t s_lo[kMaxPieces + 1];
+    __shared__ uint32_t s_psrc[kMaxPieces];
+    __shared__ uint32_t s_seg[kPipeMaxBatch][kMaxPieces + 1];
+    __shared__ unsigned long long s_fval[kPipeMaxBatch][kMaxTiles];
+    __shared__ uint32_t s_ok[kPipeMaxBatch];
+    __shared__ uint32_t s_dtmp[DW + 1];
+    __shared__ uint32_t s_wa[NPT * UW], s_wb[NPT * UW], s_mw[UW], s_out[3];
+    __shared__ uint32_t s_delivered;  // frames delivered: rel 0 .. s_delivered
+    __shared__ uint32_t s_updated;    // update steps whose fold is done
+    __shared__ unsigned long long s_prof[P_SLOTS];
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t c = blockIdx.x, C = ps.C, P = ps.P;
+    for (uint32_t j = tid; j <= P; j += NT) s_lo[j] = ps.piece_lo[j];
+    for (uint32_t j = tid; j < P; j += NT) s_psrc[j] = ps.piece_src[j];
+    for (uint32_t j = tid; j < ring_words; j += NT) ring[j] = 0;
+    if (tid < P_SLOTS) s_prof[tid] = 0;
+    if (tid == 0) {
+        s_delivered = 0;
+        s_updated = 0;
+    }
+    __syncthreads();
+    const uint32_t pa = ps.cta_piece[2 * c], pb = ps.cta_piece[2 * c + 1];
+    const uint32_t alo = s_lo[pa], na = s_lo[pa + 1] - alo;  // receiving piece
+    const uint32_t blo = s_lo[pb], nb = s_lo[pb + 1] - blo;  // update-only piece
+    auto id_of = [&](uint32_t j) { return j < na ? alo + j : blo + (j - na); };
+    // this shard's window of every row: [split[s][0], split[s][C])
+    if (ps.pf_cap)
+        for (uint32_t j = tid; j < na + nb; j += NT) {
+            const uint32_t i = id_of(j);
+            pf[j] = make_uint2(__ldg(ps.split + static_cast<uint64_t>(i) * (C + 1)) & ~3u,
+                               __ldg(ps.split + static_cast<uint64_t>(i) * (C + 1) + C));
+        }
+    __syncthreads();
+    const uint32_t R = ps.R;
+    const int64_t fbase = t0 - static_cast<int64_t>(ps.delay);  // frame of rel 0
+    const uint32_t nrel = static_cast<uint32_t>(nsteps);
+    const bool profiling = ps.prof != nullptr && (tid == 0 || tid == static_cast<uint32_t>(UT));
+    long long tp = profiling ? clock64() : 0;
+    auto mark = [&](int slot) {
+        if (profiling) {
+            const long long now = clock64();
+            s_prof[slot] += now - tp;
+            tp = now;
+        }
+    };
+
+    if (warp < static_cast<uint32_t>(UW)) {
+        // ============================================ update warps
+        const uint32_t lead = min(ps.lead, ps.delay);
+        values_t<NF> v[NPT];
+        xorshift rr[NPT];
+        bool live[NPT];
+#pragma unroll
+        for (int r = 0; r < NPT; ++r) {
+            live[r] = false;
+            const uint32_t j = tid + r * UT;
+            if (j < na + nb) load_all(ps.nf, id_of(j), v[r]);
+        }
+        unsigned long long my_spikes = 0;
+        for (uint32_t s = 0; s < nrel; ++s) {
+            const int64_t t = t0 + s;
+            const uint32_t slot = static_cast<uint32_t>(t % ps.Q);
+            uint32_t* qslot = ps.queue + static_cast<uint64_t>(slot) * ps.n;
+            // frames through rel s (needed) and s + delay - lead (pacing)
+            wait_at_least(&s_delivered, min(s + ps.delay - lead, nrel));
+            mark(P_POLL);
+            uint32_t* cslot = ring + (s % R) * ps.K * ps.win_cap;
+            bool spk[NPT];
+            uint32_t mcount = 0;
+#pragma unroll
+            for (int r = 0; r < NPT; ++r) {
+                const uint32_t j = tid + r * UT;
+                spk[r] = false;
+                if (j < na + nb) {
+                    const uint32_t i = id_of(j);
+                    if (j < na) {  // receiving neuron: fold frame rel s in class order
+                        float acc = detail::pack_get<ACC>::get(v[r]);
+                        for (int k = 0; k < ps.K; ++k) {
+                            const uint32_t a = cslot[k * ps.win_cap + j];
+                            if (a) {
+                                cslot[k * ps.win_cap + j] = 0;
+                                acc = fold_arrivals(acc, a, ps.delta[k]);
+                            }
+                        }
+                        detail::pack_get<ACC>::get(v[r]) = acc;
+                    }
+                    values_t<NF> vl = v[r];
+                    xorshift rl = rr[r];
+                    bool ll = live[r];
+                    local_neuron<NF> ref{i, &vl, &rl, &ll, ps.rng};
+                    spk[r] = model.update(ref, ps.dt);
+                    v[r] = vl;
+                    rr[r] = rl;
+                    live[r] = ll;
+                    mcount += (spk[r] && i >= ps.meas_lo && i < ps.meas_hi) ? 1u : 0u;
+                }
+                const unsigned ba = __ballot_sync(0xffffffffu, spk[r] && j < na);
+                const unsigned bb = __ballot_sync(0xffffffffu, spk[r] && j >= na);
+                if (lane == 0) {
+                    s_wa[r * UW + warp] = __popc(ba);
+                    s_wb[r * UW + warp] = __popc(bb);
+                }
+            }
+            for (int o = 16; o; o >>= 1) mcount += __shfl_xor_sync(0xffffffffu, mcount, o);
+            if (lane == 0) s_mw[warp] = mcount;
+            mark(P_UPDATE);
+            named_bar(BAR_U, UT);  // counts and the slot zeroing are complete
+            mark(8);
+            if (tid == 0) st_release_cta(&s_updated, s + 1);
+            if (warp == 0) {  // exclusive scans of the per-warp counts, ascending local index
+                uint32_t runa = 0, runb = 0;
+#pragma unroll
+                for (int r = 0; r < NPT; ++r) {
+                    const uint32_t xa = lane < UW ? s_wa[r * UW + lane] : 0;
+                    const uint32_t xb = lane < UW ? s_wb[r * UW + lane] : 0;
+                    uint32_t ia = xa, ib = xb;
+#pragma unroll
+                    for (int o = 1; o < UW; o <<= 1) {
+                        const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o);
+                        const uint32_t yb = __shfl_up_sync(0xffffffffu, ib, o);
+                        if (lane >= static_cast<uint32_t>(o)) {
+                            ia += ya;
+                            ib += yb;
+                        }
+                    }
+                    if (lane < UW) {
+                        s_wa[r * UW + lane] = runa + ia - xa;
+                        s_wb[r * UW + lane] = runb + ib - xb;
+                    }
+                    runa += __shfl_sync(0xffffffffu, ia, UW - 1);
+                    runb += __shfl_sync(0xffffffffu, ib, UW - 1);
+                }
+                uint32_t mm = lane < UW ? s_mw[lane] : 0;
+                for (int o = 16; o; o >>= 1) mm += __shfl_xor_sync(0xffffffffu, mm, o);
+                if (lane == 0) {
+                    s_out[0] = runa;
+                    s_out[1] = runb;
+                    s_out[2] = mm;
+                }
+            }
+            named_bar(BAR_U, UT);
+            mark(9);
+#pragma unroll
+            for (int r = 0; r < NPT; ++r) {
+                const uint32_t j = tid + r * UT;
+                const unsigned ba = __ballot_sync(0xffffffffu, spk[r] && j < na);
+                const unsigned bb = __ballot_sync(0xffffffffu, spk[r] && j >= na);
+                const unsigned below = (1u << lane) - 1u;
+                if (spk[r]) {
+                    if (j < na)
+                        qslot[alo + s_wa[r * UW + warp] + __popc(ba & below)] = id_of(j);
+                    else
+                        qslot[blo + s_wb[r * UW + warp] + __popc(bb & below)] = id_of(j);
+                }
+            }
+            const uint32_t outa = s_out[0], outb = s_out[1], meas = s_out[2];
+            named_bar(BAR_U, UT);  // piece slices complete (and s_out / s_w* reusable)
+            if (tid == 0) {
+                st_release_gpu(ps.finfo + static_cast<uint64_t>(slot) * ps.E + c, frame_word(t, outa, outb));
+                if (outa + outb) atomicAdd(&ps.step_spikes[s], outa + outb);
+                if (meas) atomicAdd(&ps.step_meas[s], meas);
+                my_spikes += outa + outb;
+            }
+            // stream the rows of this CTA's spikes into L2 for every deliverer
+            if (ps.pf_cap) {
+#pragma unroll
+                for (int r = 0; r < NPT; ++r) {
+                    const uint32_t j = tid + r * UT;
+                    if (spk[r]) {
+                        const uint2 w = pf[j];
+                        const uint32_t bytes = w.y > w.x ? ((w.y - w.x) * 4 + 15) & ~15u : 0;
+                        if (bytes)
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                             ps.cells + static_cast<uint64_t>(id_of(j)) * ps.pitch + w.x),
+                                         "r"(bytes)
+                                         : "memory");
+                        // ... and its receive windows (split row), read by every deliverer
+                        const uint64_t s0 = static_cast<uint64_t>(id_of(j)) * (C + 1) * 4;
+                        const uint64_t a0 = s0 & ~15ull, a1 = (s0 + (C + 1) * 4 + 15) & ~15ull;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                         reinterpret_cast<const char*>(ps.split) + a0),
+                                     "r"(static_cast<uint32_t>(a1 - a0))
+                                     : "memory");
+                    }
+                }
+            }
+            mark(P_PUBLISH);
+        }
+        named_bar(BAR_U, UT);
+        // write back the register-resident state; fold the last delivered
+        // frame (rel nsteps) into ACC so host reads and the next launch see it
+#pragma unroll
+        for (int r = 0; r < NPT; ++r) {
+            const uint32_t j = tid + r * UT;
+            if (j >= na + nb) continue;
+            if (j < na) {
+                wait_at_least(&s_delivered, nrel);
+                const uint32_t* cslot = ring + (nrel % R) * ps.K * ps.win_cap;
+                float acc = detail::pack_get<ACC>::get(v[r]);
+                for (int k = 0; k < ps.K; ++k) acc = fold_arrivals(acc, cslot[k * ps.win_cap + j], ps.delta[k]);
+                detail::pack_get<ACC>::get(v[r]) = acc;
+            }
+            const uint32_t i = id_of(j);
+            store_all(ps.nf, i, v[r]);
+            if constexpr (model_uses_rng<M>())
+                if (live[r]) ps.rng[i] = rr[r];
+        }
+        if (tid == 0 && my_spikes) atomicAdd(&ps.counters[C_SPIKES], my_spikes);
+        if (profiling) s_prof[P_STEPS] = static_cast<unsigned long long>(nsteps);
+    } else {
+        // ============================================ delivery warps
+        const uint32_t dtid = tid - UT, dwarp = warp - UW;
+        unsigned long long my_deliv = 0;
+        unsigned long long lc = 0;  // CTA 0: log cursor
+        const bool log_cta = ps.log && c == 0;
+        const uint4* cells4 = reinterpret_cast<const uint4*>(ps.cells);
+        const uint32_t pitch4 = ps.pitch >> 2;
+        const uint32_t cap = ps.stage_items;
+        uint32_t r_next = 1;
+        // frames before 0 do not exist: nothing to deliver (engine.hpp:371-380)
+        if (fbase + 1 < 0) {
+            const int64_t last_neg = -1 - fbase;  // rel of frame -1
+            r_next = static_cast<uint32_t>(min(last_neg, static_cast<int64_t>(nrel))) + 1;
+            if (dtid == 0) st_release_cta(&s_delivered, r_next - 1);
+        }
+        while (r_next <= nrel) {
+            // ---- poll: warp w takes frame rel r_next + w (warp 0 waits)
+            // (frame f is taken once frame f + lag is complete: the
+            // publishers streamed the rows of f into L2 meanwhile)
+            if (dwarp < static_cast<uint32_t>(kPipeMaxBatch)) {
+                const uint32_t r = r_next + dwarp;
+                bool ok = false;
+                if (dwarp == 0) {
+                    // ring slot r % R is free once update step r - R folded it
+                    if (r >= R) wait_at_least(&s_updated, r - R + 1);
+                    if (ps.lag) frame_complete(ps, fbase + r + ps.lag, true);
+                    if (profiling) mark(6);
+                    ok = frame_prefix(ps, fbase + r, s_seg[0], s_fval[0], s_psrc, false);
+                } else if (r <= nrel && r + 1 <= ld_acquire_cta(&s_updated) + R &&
+                           (ps.lag == 0 || frame_complete(ps, fbase + r + ps.lag, false))) {
+                    ok = frame_prefix(ps, fbase + r, s_seg[dwarp], s_fval[dwarp], s_psrc, true);
+                }
+                if (lane == 0) s_ok[dwarp] = ok ? 1u : 0u;
+            }
+            named_bar(BAR_D, DT);
+            if (profiling) mark(10);
+            uint32_t B = 0;
+            uint32_t fpre[kPipeMaxBatch + 1];
+            fpre[0] = 0;
+#pragma unroll
+            for (int w = 0; w < kPipeMaxBatch; ++w) {
+                const bool take = (static_cast<uint32_t>(w) == B) && s_ok[w];
+                if (take) ++B;
+                fpre[w + 1] = fpre[w] + (take ? s_seg[w][P] : 0u);
+            }
+            const uint32_t S = fpre[B];
+            // CTA 0 logs the frames >= log_from of this pass, in order
+            uint32_t wlog = B;
+            if (log_cta) {
+                const int64_t d = ps.log_from - (fbase + r_next);
+                wlog = d <= 0 ? 0u : static_cast<uint32_t>(min(d, static_cast<int64_t>(B)));
+            }
+            uint32_t flog = 0;
+#pragma unroll
+            for (int q = 1; q <= kPipeMaxBatch; ++q)
+                if (static_cast<uint32_t>(q) == wlog) flog = fpre[q];
+            const unsigned long long lbase = lc - flog;
+            for (uint32_t g0 = 0; g0 < S; g0 += DT) {
+                // one spike per thread: id, this CTA's row window, chunk count
+                const uint32_t g = g0 + dtid;
+                uint32_t nchunk = 0, sb = 0, se = 0, base = 0, row4 = 0;
+                if (g < S) {
+                    uint32_t w = 0, fw = 0;
+#pragma unroll
+                    for (int q = 1; q < kPipeMaxBatch; ++q)
+                        if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
+                            w = q;
+                            fw = fpre[q];
+                        }
+                    const uint32_t gl = g - fw;
+                    const uint32_t* seg = s_seg[w];
+                    const uint32_t a = piece_of(seg, P, gl);
+                    const int64_t f = fbase + r_next + w;
+                    const uint32_t src =
+                        __ldcg(ps.queue + static_cast<uint64_t>(f % ps.Q) * ps.n + s_lo[a] + (gl - seg[a]));
+                    if (w >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src;
+                    const uint32_t* sp = ps.split + static_cast<uint64_t>(src) * (C + 1) + c;
+                    sb = __ldg(sp);
+                    se = __ldg(sp + 1);
+                    my_deliv += se - sb;
+                    row4 = src * pitch4;
+                    base = (((r_next + w) % R) * ps.K + static_cast<uint32_t>(source_class(ps, src))) * ps.win_cap;
+                    nchunk = se > sb ? ((se + 3) >> 2) - (sb >> 2) : 0;
+                }
+                uint32_t total;
+                const uint32_t first = group_exclusive_scan<DT, UW, BAR_D>(nchunk, s_dtmp, total);
+                if (profiling) mark(P_GATHER);
+                for (uint32_t i0 = 0; i0 < total; i0 += cap) {
+                    // chunk list: {16-byte chunk index, ring base << 5 | hi << 2 | lo}
+                    for (uint32_t q = 0; q < nchunk; ++q) {
+                        const uint32_t it = first + q;
+                        if (it < i0 || it >= i0 + cap) continue;
+                        const uint32_t w0 = ((sb >> 2) + q) << 2;  // first word of the chunk
+                        const uint32_t lo = sb > w0 ? sb - w0 : 0;
+                        const uint32_t hi = min(4u, se - w0);
+                        chunks[it - i0] = make_uint2(row4 + (sb >> 2) + q, (base << 5) | (hi << 2) | lo);
+                    }
+                    named_bar(BAR_D, DT);
+                    if (profiling) mark(11);
+                    const uint32_t m = min(cap, total - i0);
+                    for (uint32_t k0 = dtid; k0 < m; k0 += kChunkBatch * DT) {
+                        uint2 d[kChunkBatch];
+                        uint4 x[kChunkBatch];
+#pragma unroll
+                        for (int u = 0; u < kChunkBatch; ++u) {
+                            const uint32_t k = k0 + u * DT;
+                            d[u] = k < m ? chunks[k] : make_uint2(0, 0);
+                        }
+#pragma unroll
+                        for (int u = 0; u < kChunkBatch; ++u)
+                            x[u] = d[u].y ? ldg_stream4(cells4 + d[u].x) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                        for (int u = 0; u < kChunkBatch; ++u) {
+                            const uint32_t lo = d[u].y & 3u, hi = (d[u].y >> 2) & 7u;
+                            uint32_t* cb = ring + (d[u].y >> 5) - alo;
+                            if (lo == 0 && hi > 0) atomicAdd(cb + x[u].x, 1u);
+                            if (lo <= 1 && hi > 1) atomicAdd(cb + x[u].y, 1u);
+                            if (lo <= 2 && hi > 2) atomicAdd(cb + x[u].z, 1u);
+                            if (hi > 3) atomicAdd(cb + x[u].w, 1u);
+                        }
+                    }
+                    named_bar(BAR_D, DT);
+                }
+                if (profiling) mark(P_DELIVER);
+            }
+            if (wlog < B) lc = lbase + S;
+            // every counting atomic of the pass precedes the release (barrier)
+            if (S == 0) named_bar(BAR_D, DT);
+            if (dtid == 0) st_release_cta(&s_delivered, r_next + B - 1);
+            if (profiling) s_prof[7] += 1;
+            r_next += B;
+        }
+        for (int o = 16; o; o >>= 1) my_deliv += __shfl_xor_sync(0xffffffffu, my_deliv, o);
+        if (lane == 0 && my_deliv) atomicAdd(&ps.counters[C_DELIVERIES], my_deliv);
+        if (log_cta && dtid == 0) {
+            *ps.log_end = lc;
+            if (lc > ps.log_cap) ps.flags[0] = 1;
+        }
+    }
+    __syncthreads();
+    if (ps.prof != nullptr && tid < P_SLOTS) atomicAdd(&ps.prof[c * P_SLOTS + tid], s_prof[tid]);
+}
+
+}  // namespace synq::dev

@@ -32,6 +32,7 @@
 #include <array>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -46,6 +47,7 @@
 #include "synq/detail/device_graph.hpp"
 #include "synq/detail/kernels.cuh"
 #include "synq/detail/persistent.cuh"
+#include "synq/detail/pipeline.cuh"
 #include "synq/models/benchmarks.hpp"
 #include "synq/network_desc.hpp"
 #include "synq/random.hpp"
@@ -65,6 +67,8 @@ struct engine_options {
     int persistent = -1;       // -1 auto, 0 never, 1 require (population-delivery models)
     uint32_t tiles = 0;        // persistent CTAs (0 = auto)
     bool profile = false;      // per-phase cycle counters in the persistent kernel
+    int pipeline = -1;         // persistent kernel: -1 auto (pipelined when it fits), 0 serial, 1 pipelined
+    uint32_t lead = 0;         // pipelined: frames the update may run ahead of delivery (0 = auto)
     // target-partitioned multi-GPU shard: this process owns
     // shard_rank of shard_world; frames are exchanged with export/import
     uint32_t shard_rank = 0;
@@ -302,6 +306,7 @@ public:
     bool deterministic() const { return opt_.deterministic; }
     unsigned worker_count() const { return persistent_ ? tiles_ : static_cast<unsigned>(sms_); }
     bool persistent() const { return persistent_; }
+    bool pipelined() const { return persistent_ && pipe_; }
     bool exact() const { return exact_ || persistent_; }
     uint64_t construction_fixups() const { return graph_.tie_fixups; }
     // device time of all run() calls (CUDA events on the engine stream) and of
@@ -396,6 +401,9 @@ public:
         for (int k = 0; k < 5; ++k) out[5 + k] = h[crit * dev::P_SLOTS + k] / steps;
         out[10] = h[crit * dev::P_SLOTS + 6] / steps;
         out[11] = h[crit * dev::P_SLOTS + 7] / steps;
+        out[12] = h[crit * dev::P_SLOTS + 8] / steps;
+        out[13] = h[crit * dev::P_SLOTS + 9] / steps;
+        out[14] = (h[crit * dev::P_SLOTS + 10] + h[crit * dev::P_SLOTS + 11]) / steps;
         return out;
     }
 
@@ -612,7 +620,8 @@ private:
             longest = std::max(longest, (alo[c + 1] - alo[c]) + (blo[c + 1] - blo[c]));
             wcap = std::max(wcap, alo[c + 1] - alo[c]);
         }
-        if (longest > max_local) return;  // cannot hold the state: per-step kernel graph
+        const bool pipe_fits = longest <= 2048 && uint64_t(n_) * (graph_.pitch / 4) < (1ull << 32);
+        if (longest > max_local && !pipe_fits) return;  // cannot hold the state: per-step kernel graph
         npt_ = longest <= NTH ? 1 : (longest <= 2 * NTH ? 2 : 4);
         // pieces in id order; publishers: local CTAs 0..C-1, then remote shards
         const uint32_t E = C + W - 1;
@@ -646,20 +655,30 @@ private:
         piece_lo.push_back(n_);
         for (uint32_t p = 0; p + 1 < piece_lo.size(); ++p)  // pieces must tile the id space in order
             if (piece_lo[p] > piece_lo[p + 1]) throw device_error("internal: shard pieces out of order");
-        // dynamic smem: counts only (delivery items are static)
         int max_smem = 0, dev = 0;
         SYNQ_CUDA(cudaGetDevice(&dev));
         SYNQ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const size_t static_smem = 3 * (dev::kMaxPieces + 1) * 4 + 8192;
-        const size_t counts = ((size_t(K) * wcap + 31) & ~size_t(31)) * 4;
-        if (counts + static_smem + 1024 * 16 > size_t(max_smem)) return;
-        // the rest of shared memory holds the 16-byte chunk list (16 B per chunk)
-        const size_t chunk_cap = std::min<size_t>(16384, (size_t(max_smem) - static_smem - counts) / 16);
-        const size_t smem = counts + chunk_cap * 16;
-        stage_items_ = static_cast<uint32_t>(chunk_cap);
+        size_t smem = 0;
+        if (!setup_pipeline(K, wcap, longest, delay_, size_t(max_smem), smem)) {
+            if (longest > max_local) return;
+            // dynamic smem: counts only (delivery items are static)
+            const size_t static_smem = 3 * (dev::kMaxPieces + 1) * 4 + 8192;
+            const size_t counts = ((size_t(K) * wcap + 31) & ~size_t(31)) * 4;
+            if (counts + static_smem + 1024 * 16 > size_t(max_smem)) return;
+            // the rest of shared memory holds the 16-byte chunk list (16 B per chunk)
+            const size_t chunk_cap = std::min<size_t>(16384, (size_t(max_smem) - static_smem - counts) / 16);
+            smem = counts + chunk_cap * 16;
+            stage_items_ = static_cast<uint32_t>(chunk_cap);
+        }
         npt_select_ = npt_;
-        const void* fn = persistent_fn();
-        SYNQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        const void* fn = kernel_fn();
+        {   // the attribute is per kernel, shared by every network in the process:
+            // always the maximum, so a smaller network never shrinks a larger one's
+            cudaFuncAttributes fa{};
+            SYNQ_CUDA(cudaFuncGetAttributes(&fa, fn));
+            SYNQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           max_smem - static_cast<int>(fa.sharedSizeBytes)));
+        }
         int per_sm = 0;
         SYNQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, dev::kPersistThreads, smem));
         if (per_sm < 1) return;
@@ -762,6 +781,90 @@ private:
         return s;
     }
 
+    // Pipelined kernel (detail/pipeline.cuh) when the options allow it and it
+    // fits: UW update warps hold <= 8 neurons per thread in registers; shared
+    // memory holds a count ring of R <= delay frames, the row prefetch windows
+    // and the chunk list.  Sets pipe_* and stage_items_; false = serial kernel.
+    bool setup_pipeline(int K, uint32_t wcap, uint32_t longest, uint32_t delay, size_t max_smem, size_t& smem)
+        requires population_model {
+        pipe_ = false;
+        int mode = opt_.pipeline;
+        if (const char* e = std::getenv("SYNQ_PIPELINE")) mode = std::atoi(e);
+        if (mode == 0) return false;
+        if (uint64_t(n_) * (graph_.pitch / 4) >= (1ull << 32)) return false;  // 32-bit chunk indices
+        uint32_t uw_pref = 4;
+        if (const char* e = std::getenv("SYNQ_UW")) uw_pref = std::atoi(e) == 8 ? 8 : 4;
+        if (uw_pref == 8 && longest <= 8 * 32 * 8) {
+            pipe_uw_ = 8;
+            pipe_npt_ = longest <= 256 ? 1 : (longest <= 512 ? 2 : (longest <= 1024 ? 4 : 8));
+        } else if (longest <= 4 * 32 * 8) {
+            pipe_uw_ = 4;
+            pipe_npt_ = longest <= 128 ? 1 : (longest <= 256 ? 2 : (longest <= 512 ? 4 : 8));
+        } else if (longest <= 8 * 32 * 8) {
+            pipe_uw_ = 8;
+            pipe_npt_ = 8;
+        } else {
+            return false;
+        }
+        pipe_ = true;
+        cudaFuncAttributes attr{};
+        SYNQ_CUDA(cudaFuncGetAttributes(&attr, kernel_fn()));
+        const size_t avail = max_smem > attr.sharedSizeBytes ? max_smem - attr.sharedSizeBytes : 0;
+        // L2 row prefetch pays once the adjacency outgrows L2
+        bool prefetch = graph_.pitch * 4ull * n_ > (64ull << 20);
+        if (const char* e = std::getenv("SYNQ_PREFETCH")) prefetch = std::atoi(e) != 0;
+        const uint32_t pf_cap = prefetch ? ((longest + 1) & ~1u) : 0;
+        const size_t slot_bytes = size_t(K) * wcap * 4;
+        const size_t fixed = size_t(pf_cap) * 8 + 2048 * 8 + 16;  // prefetch windows + a minimal chunk list
+        if (avail <= fixed || slot_bytes == 0) {
+            pipe_ = false;
+            return false;
+        }
+        uint64_t R = std::min<uint64_t>(delay, (avail - fixed) / slot_bytes);
+        while (R > 0 && R * K * wcap >= (1ull << 27)) --R;  // ring offsets are 27-bit in the chunk list
+        if (R < 1) {
+            pipe_ = false;
+            return false;
+        }
+        // delivery lag (frames) behind publication: rows prefetched at publish
+        // reach L2 before they are delivered; lead > lag avoids a deadlock
+        uint32_t lag = prefetch ? 1 : 0;
+        if (const char* e = std::getenv("SYNQ_LAG")) lag = static_cast<uint32_t>(std::max(0, std::atoi(e)));
+        lag = std::min(lag, delay - 1);
+        uint32_t lead = opt_.lead ? opt_.lead : lag + 4;
+        if (const char* e = std::getenv("SYNQ_LEAD")) lead = static_cast<uint32_t>(std::max(1, std::atoi(e)));
+        lead = std::max(lead, lag + 1);
+        const size_t ring_bytes = ((R * K * wcap + 3) & ~uint64_t(3)) * 4;
+        const size_t chunk_cap = std::min<size_t>(16384, (avail - ring_bytes - size_t(pf_cap) * 8) / 8);
+        smem = ring_bytes + size_t(pf_cap) * 8 + chunk_cap * 8;
+        stage_items_ = static_cast<uint32_t>(chunk_cap);
+        ring_R_ = static_cast<uint32_t>(R);
+        lead_ = std::max<uint32_t>(1, std::min(lead, delay));
+        lag_ = lag;
+        pf_cap_ = pf_cap;
+        return true;
+    }
+
+    const void* kernel_fn() const requires population_model {
+        if (pipe_) {
+            if (pipe_uw_ == 8) {
+                switch (pipe_npt_) {
+                    case 1: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 1>);
+                    case 2: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 2>);
+                    case 4: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 4>);
+                    default: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 8>);
+                }
+            }
+            switch (pipe_npt_) {
+                case 1: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 1>);
+                case 2: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 2>);
+                case 4: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 4>);
+                default: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 8>);
+            }
+        }
+        return persistent_fn();
+    }
+
     const void* persistent_fn() const requires population_model {
         switch (npt_) {
             case 1: return reinterpret_cast<const void*>(dev::k_persistent<Model, 1>);
@@ -805,6 +908,10 @@ private:
         p.win_cap = win_cap_;
         p.stage_items = stage_items_;
         p.prof = prof_ ? prof_.get() : nullptr;
+        p.R = ring_R_;
+        p.lead = lead_;
+        p.pf_cap = pf_cap_;
+        p.lag = lag_;
         return p;
     }
 
@@ -856,7 +963,7 @@ private:
                 int32_t nsteps = static_cast<int32_t>(b);
                 Model m = model_;
                 void* args[] = {&m, &ps, &t0, &nsteps};
-                SYNQ_CUDA(cudaLaunchCooperativeKernel(persistent_fn(), dim3(tiles_),
+                SYNQ_CUDA(cudaLaunchCooperativeKernel(kernel_fn(), dim3(tiles_),
                                                       dim3(dev::kPersistThreads), args, smem_, stream_));
                 launches_ += 1;
             }
@@ -1066,6 +1173,8 @@ private:
     int64_t last_batch_t0_ = 0;
     uint32_t last_batch_b_ = 0;
     int npt_select_ = 1;
+    bool pipe_ = false;  // pipelined kernel (detail/pipeline.cuh)
+    uint32_t pipe_uw_ = 4, pipe_npt_ = 1, ring_R_ = 0, lead_ = 0, lag_ = 0, pf_cap_ = 0;
     size_t smem_ = 0;
     int npt_ = 1;
     dev_array<unsigned long long> prof_;

@@ -114,6 +114,7 @@ def lib() -> C.CDLL:
     sig("synq_opts_batch_steps", st, vp, u32)
     sig("synq_opts_persistent", st, vp, C.c_int)
     sig("synq_opts_tiles", st, vp, u32)
+    sig("synq_opts_pipeline", st, vp, C.c_int, u32)
     sig("synq_sim_engine", C.c_int, vp)
     sig("synq_sim_exact", C.c_int, vp)
     sig("synq_sim_counters", st, vp, vp)
@@ -154,7 +155,7 @@ class Opts:
 
     def __init__(self, seed=None, threads=None, deterministic=None, dt=None, delay=None,
                  record=None, defaults_file=None, params=None, batch_steps=None,
-                 persistent=None, tiles=None, profile=None, shard=None):
+                 persistent=None, tiles=None, profile=None, shard=None, pipeline=None, lead=0):
         self.h = lib().synq_opts_new()
         if not self.h:
             raise MemoryError("synq_opts_new")
@@ -181,6 +182,8 @@ class Opts:
             check(L.synq_opts_persistent(self.h, persistent))
         if tiles is not None:
             check(L.synq_opts_tiles(self.h, tiles))
+        if pipeline is not None:
+            check(L.synq_opts_pipeline(self.h, int(pipeline), int(lead)))
         if profile is not None:
             check(L.synq_opts_profile(self.h, int(profile)))
         if shard is not None:
@@ -268,6 +271,10 @@ class Sim:
     @property
     def persistent(self) -> bool:
         return bool(lib().synq_sim_engine(self.h))
+
+    @property
+    def pipelined(self) -> bool:
+        return lib().synq_sim_engine(self.h) == 2
 
     @property
     def exact(self) -> bool:
@@ -358,7 +365,9 @@ class Sim:
              "pacing": dict(zip(names, (round(float(x)) for x in out[5:10]))),
              "update_detail": {"own_work": round(float(out[10])), "to_first_barrier": round(float(out[11]))},
              "producer": dict(zip(["poll", "ids", "splits", "rebase", "issue"],
-                                  (round(float(x)) for x in out[10:15]))), "tiles": tiles.value}
+                                  (round(float(x)) for x in out[10:15]))),
+             "pipeline": dict(zip(["deliver_wait", "passes", "update_bar1", "update_scan", "prefix_chunklist"],
+                                  (round(float(x), 2) for x in out[10:15]))), "tiles": tiles.value}
         return d
 
     # ---- multi-GPU shard exchange

@@ -60,6 +60,7 @@ public:
     virtual int64_t warmup_steps() const = 0;
     virtual const spike_raster& raster() const = 0;
     virtual bool persistent() const = 0;
+    virtual bool pipelined() const = 0;
     virtual bool exact() const = 0;
     virtual const std::vector<uint32_t>& step_spikes() const = 0;
     virtual void neuron_field_bytes(uint32_t f, void* out, uint64_t bytes) = 0;
@@ -186,6 +187,7 @@ public:
     int64_t warmup_steps() const override { return warmup_; }
     const spike_raster& raster() const override { return raster_; }
     bool persistent() const override { return net_->persistent(); }
+    bool pipelined() const override { return net_->pipelined(); }
     bool exact() const override { return net_->exact(); }
     const std::vector<uint32_t>& step_spikes() const override { return net_->step_spike_counts(); }
     void neuron_field_bytes(uint32_t f, void* out, uint64_t bytes) override {
@@ -258,7 +260,7 @@ void sim_base::write_stats(std::ostream& out) const {
             << "\n";
     } catch (const std::invalid_argument&) {
     }
-    out << "engine=" << (persistent() ? "b200-persistent" : "b200-graph") << "\n"
+    out << "engine=" << (pipelined() ? "b200-pipelined" : (persistent() ? "b200-persistent" : "b200-graph")) << "\n"
         << "exact=" << (exact() ? 1 : 0) << "\n";
     out.flush();
 }
@@ -687,6 +689,16 @@ synq_status synq_sim_shard_import(synq_sim* s, const void* src, uint64_t words, 
         return SYNQ_OK;
     });
 }
+synq_status synq_opts_pipeline(synq_opts* o, int mode, uint32_t lead) {
+    SYNQ_CHECK_HANDLE(o);
+    if (mode < -1 || mode > 1) {
+        set_error("pipeline mode must be -1, 0 or 1");
+        return SYNQ_ERR_INVALID_ARGUMENT;
+    }
+    o->cfg.engine.pipeline = mode;
+    o->cfg.engine.lead = lead;
+    return SYNQ_OK;
+}
 synq_status synq_opts_profile(synq_opts* o, int on) {
     SYNQ_CHECK_HANDLE(o);
     o->cfg.engine.profile = on != 0;
@@ -702,7 +714,10 @@ synq_status synq_sim_phase_cycles(const synq_sim* s, double out[15], uint32_t* t
         return SYNQ_OK;
     });
 }
-int synq_sim_engine(const synq_sim* s) { return s && s->impl->persistent() ? 1 : 0; }
+int synq_sim_engine(const synq_sim* s) {
+    if (!s || !s->impl->persistent()) return 0;
+    return s->impl->pipelined() ? 2 : 1;
+}
 int synq_sim_exact(const synq_sim* s) { return s && s->impl->exact() ? 1 : 0; }
 
 synq_status synq_sim_counters(const synq_sim* s, uint64_t out[6]) {
