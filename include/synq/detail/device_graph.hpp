@@ -46,4 +46,11 @@ std::vector<uint32_t> in_degrees(const device_graph& g, cudaStream_t stream);
 void build_splits(const device_graph& g, const std::vector<uint32_t>& tile_lo,
                   dev_array<uint32_t>& split, cudaStream_t stream);
 
+// receive-window bitmaps for the bitmap delivery of the pipelined engine:
+// bm[s * C * wq + c * wq + q] (uint4) holds bits 128q .. 128q+127 of window c
+// ([window_lo[c], window_hi[c]) target ids, at most 128 * wq wide) of row s
+void build_window_bitmaps(const device_graph& g, const std::vector<uint32_t>& window_lo,
+                          const std::vector<uint32_t>& window_hi, uint32_t wq, dev_array<uint4>& bm,
+                          cudaStream_t stream);
+
 }  // namespace synq

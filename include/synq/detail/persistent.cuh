@@ -92,6 +92,11 @@ struct persist_state {
     uint32_t lead;    // update runs at most this many frames ahead of local delivery
     uint32_t pf_cap;  // row-prefetch windows held in smem (0: no L2 row prefetch)
     uint32_t lag;     // frame f is delivered once frame f + lag is complete (its rows are in L2)
+    // bitmap delivery: row s = C windows of wq uint4 (bits of targets window_lo + k)
+    const uint4* bm;
+    uint32_t bm_row4;      // uint4 per bitmap row (= C * wq)
+    uint32_t wq;           // uint4 per window (1, 2, 4 or 8)
+    uint32_t bm_prefetch;  // stream the bitmap rows of published spikes into L2
 };
 
 // streaming 16-byte read of adjacency cells: read-only, no L1 allocation
@@ -124,14 +129,15 @@ SYNQ_DEV int source_class(const persist_state<M>& ps, uint32_t src) {
 // re-add the per-class increments in ascending class (= ascending source id)
 // order: the reference's float summation, one rounding per arrival
 SYNQ_DEV float fold_arrivals(float acc, uint32_t n, float d) {
-    uint32_t q = 0;
-    for (; q + 4 <= n; q += 4) {
+#pragma unroll 1
+    for (; n >= 4; n -= 4) {
         acc = acc + d;
         acc = acc + d;
         acc = acc + d;
         acc = acc + d;
     }
-    for (; q < n; ++q) acc = acc + d;
+#pragma unroll 1
+    for (; n; --n) acc = acc + d;
     return acc;
 }
 
@@ -234,12 +240,13 @@ SYNQ_DEV bool frame_prefix(const persist_state<M>& ps, int64_t f, uint32_t* seg,
     return true;
 }
 
-// Warp-wide: is frame f published by every publisher (blocking: wait)?
+// Warp-wide: is frame f published by the first E publishers (blocking:
+// wait)?  The local CTAs are publishers 0 .. C-1, remote shards follow.
 template <class M>
-SYNQ_DEV bool frame_complete(const persist_state<M>& ps, int64_t f, bool blocking) {
-    const uint32_t lane = threadIdx.x & 31, E = ps.E;
+SYNQ_DEV bool frame_complete(const persist_state<M>& ps, int64_t f, bool blocking, uint32_t E) {
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t want = frame_tag(f);
-    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(f % ps.Q) * E;
+    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(f % ps.Q) * ps.E;
     bool ok = true;
     for (uint32_t j = lane; j < E; j += 32) {
         if (blocking) {

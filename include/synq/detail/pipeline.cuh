@@ -36,7 +36,8 @@
 // * update(t) waits until frame t - min(lead, delay) is delivered locally.
 //   This is needed for t - delay.  The lead bounds how far the update can
 //   run ahead, so the rows it prefetched are still in L2 when they are
-//   delivered;
+//   delivered.  The wait never reaches past frame t - delay + R - 1: that
+//   frame's ring slot is only freed by update(t) itself;
 // * delivering frame f into slot f mod R waits until update(f - R + delay)
 //   folded (and zeroed) that slot's previous frame;
 // * the queue ring (Q = 2*delay slots) is never overwritten before every CTA
@@ -104,8 +105,30 @@ SYNQ_DEV uint32_t group_exclusive_scan(uint32_t x, uint32_t* s_tmp, uint32_t& to
     return r;
 }
 
-// UW update warps (NPT neurons per update thread); the other warps deliver
-template <class M, int UW, int NPT>
+// 32x32 bit transpose across a warp: lane i holds row i on entry, lane b
+// holds column b on exit (bit i = bit b of lane i's entry word).  Stages 16
+// and 8 are byte permutes, stages 4 / 2 / 1 a rotate plus a masked merge.
+SYNQ_DEV uint32_t transpose32(uint32_t x, uint32_t lane) {
+    uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16);
+    x = __byte_perm(x, y, (lane & 16) ? 0x3276u : 0x5410u);
+    y = __shfl_xor_sync(0xffffffffu, x, 8);
+    x = __byte_perm(x, y, (lane & 8) ? 0x3715u : 0x6240u);
+#pragma unroll
+    for (int j = 4; j >= 1; j >>= 1) {
+        const uint32_t m = j == 4 ? 0x0f0f0f0fu : (j == 2 ? 0x33333333u : 0x55555555u);
+        const bool hi = (lane & j) != 0;
+        y = __shfl_xor_sync(0xffffffffu, x, j);
+        const uint32_t t = __funnelshift_l(y, y, hi ? 32 - j : j);
+        const uint32_t keep = hi ? ~m : m;
+        x = (x & keep) | (t & ~keep);
+    }
+    return x;
+}
+
+// UW update warps (NPT neurons per update thread); the other warps deliver.
+// BM: bitmap delivery (receive-window bitmaps + transposed counting), else
+// 16-byte ELL row chunks counted with one shared-memory atomic per delivery.
+template <class M, int UW, int NPT, bool BM>
 __global__ void __launch_bounds__(kPipeThreads, 1)
     k_pipeline(M model, persist_state<M> ps, int64_t t0, int32_t nsteps) {
     using NF = typename M::neuron_fields;
@@ -184,8 +207,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
             const int64_t t = t0 + s;
             const uint32_t slot = static_cast<uint32_t>(t % ps.Q);
             uint32_t* qslot = ps.queue + static_cast<uint64_t>(slot) * ps.n;
-            // frames through rel s (needed) and s + delay - lead (pacing)
-            wait_at_least(&s_delivered, min(s + ps.delay - lead, nrel));
+            // frames through rel s (needed) and s + delay - lead (pacing);
+            // never beyond rel s + R - 1, whose ring slot this step frees
+            wait_at_least(&s_delivered, min(min(s + ps.delay - lead, s + R - 1), nrel));
             mark(P_POLL);
             uint32_t* cslot = ring + (s % R) * ps.K * ps.win_cap;
             bool spk[NPT];
@@ -198,13 +222,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
                     const uint32_t i = id_of(j);
                     if (j < na) {  // receiving neuron: fold frame rel s in class order
                         float acc = detail::pack_get<ACC>::get(v[r]);
-                        for (int k = 0; k < ps.K; ++k) {
-                            const uint32_t a = cslot[k * ps.win_cap + j];
-                            if (a) {
+                        uint32_t a[kMaxClasses];
+#pragma unroll
+                        for (int k = 0; k < kMaxClasses; ++k) a[k] = k < ps.K ? cslot[k * ps.win_cap + j] : 0u;
+#pragma unroll
+                        for (int k = 0; k < kMaxClasses; ++k)
+                            if (a[k]) {
                                 cslot[k * ps.win_cap + j] = 0;
-                                acc = fold_arrivals(acc, a, ps.delta[k]);
+                                acc = fold_arrivals(acc, a[k], ps.delta[k]);
                             }
-                        }
                         detail::pack_get<ACC>::get(v[r]) = acc;
                     }
                     values_t<NF> vl = v[r];
@@ -285,7 +311,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
                 my_spikes += outa + outb;
             }
             // stream the rows of this CTA's spikes into L2 for every deliverer
-            if (ps.pf_cap) {
+            if (BM && ps.bm_prefetch) {
+#pragma unroll
+                for (int r = 0; r < NPT; ++r)
+                    if (spk[r])
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                         ps.bm + static_cast<uint64_t>(id_of(tid + r * UT)) * ps.bm_row4),
+                                     "r"(ps.bm_row4 * 16)
+                                     : "memory");
+            } else if (ps.pf_cap) {
 #pragma unroll
                 for (int r = 0; r < NPT; ++r) {
                     const uint32_t j = tid + r * UT;
@@ -356,11 +390,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
                 if (dwarp == 0) {
                     // ring slot r % R is free once update step r - R folded it
                     if (r >= R) wait_at_least(&s_updated, r - R + 1);
-                    if (ps.lag) frame_complete(ps, fbase + r + ps.lag, true);
+                    if (ps.lag) frame_complete(ps, fbase + r + ps.lag, true, ps.C);  // local publishers only
                     if (profiling) mark(6);
                     ok = frame_prefix(ps, fbase + r, s_seg[0], s_fval[0], s_psrc, false);
                 } else if (r <= nrel && r + 1 <= ld_acquire_cta(&s_updated) + R &&
-                           (ps.lag == 0 || frame_complete(ps, fbase + r + ps.lag, false))) {
+                           (ps.lag == 0 || frame_complete(ps, fbase + r + ps.lag, false, ps.C))) {
                     ok = frame_prefix(ps, fbase + r, s_seg[dwarp], s_fval[dwarp], s_psrc, true);
                 }
                 if (lane == 0) s_ok[dwarp] = ok ? 1u : 0u;
@@ -388,73 +422,170 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
             for (int q = 1; q <= kPipeMaxBatch; ++q)
                 if (static_cast<uint32_t>(q) == wlog) flog = fpre[q];
             const unsigned long long lbase = lc - flog;
-            for (uint32_t g0 = 0; g0 < S; g0 += DT) {
-                // one spike per thread: id, this CTA's row window, chunk count
-                const uint32_t g = g0 + dtid;
-                uint32_t nchunk = 0, sb = 0, se = 0, base = 0, row4 = 0;
-                if (g < S) {
-                    uint32_t w = 0, fw = 0;
+            if constexpr (BM) {
+                // ---- bitmap delivery: per spike, this CTA's receive window is
+                // WQ x 128 bits of the spike's bitmap row.  Stage the windows of
+                // the pass in shared memory, then count arrivals per (frame,
+                // class, target) with warp bit-transposes + popc: one counting
+                // atomic per 32 targets x 32 spikes instead of one per delivery.
+                const uint32_t WQ = ps.wq;
+                uint4* sw = reinterpret_cast<uint4*>(chunks);  // cap x WQ, 16-byte slots swizzled
+                uint32_t* s_src = reinterpret_cast<uint32_t*>(sw + cap * WQ);
+                uint8_t* s_grp = reinterpret_cast<uint8_t*>(s_src + cap);
+                const uint32_t swz_sh = WQ == 2 ? 2u : (WQ == 4 ? 1u : 0u);
+                const uint32_t swz_m = WQ == 1 ? 0u : (WQ == 2 ? 1u : (WQ == 4 ? 3u : 7u));
+                const uint4* bmw = ps.bm + static_cast<uint64_t>(c) * WQ;
+                for (uint32_t g0 = 0; g0 < S; g0 += cap) {
+                    const uint32_t n = min(cap, S - g0);
+                    // (1) spike ids and (frame, class) groups
+                    for (uint32_t i = dtid; i < n; i += DT) {
+                        const uint32_t g = g0 + i;
+                        uint32_t w = 0, fw = 0;
 #pragma unroll
-                    for (int q = 1; q < kPipeMaxBatch; ++q)
-                        if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
-                            w = q;
-                            fw = fpre[q];
+                        for (int q = 1; q < kPipeMaxBatch; ++q)
+                            if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
+                                w = q;
+                                fw = fpre[q];
+                            }
+                        const uint32_t gl = g - fw;
+                        const uint32_t* seg = s_seg[w];
+                        const uint32_t a = piece_of(seg, P, gl);
+                        const int64_t f = fbase + r_next + w;
+                        const uint32_t src =
+                            __ldcg(ps.queue + static_cast<uint64_t>(f % ps.Q) * ps.n + s_lo[a] + (gl - seg[a]));
+                        if (w >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src;
+                        s_src[i] = src;
+                        s_grp[i] = static_cast<uint8_t>(w * 4 + static_cast<uint32_t>(source_class(ps, src)));
+                    }
+                    named_bar(BAR_D, DT);
+                    if (profiling) mark(P_GATHER);
+                    // (2) windows -> shared memory (4 loads in flight per thread)
+                    const uint32_t items = n * WQ;
+                    for (uint32_t i0 = dtid; i0 < items; i0 += 4 * DT) {
+                        uint4 v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t it = i0 + u * DT;
+                            if (it < items) {
+                                const uint32_t g = it / WQ, q = it - g * WQ;
+                                v[u] = ldg_stream4(bmw + static_cast<uint64_t>(s_src[g]) * ps.bm_row4 + q);
+                            }
                         }
-                    const uint32_t gl = g - fw;
-                    const uint32_t* seg = s_seg[w];
-                    const uint32_t a = piece_of(seg, P, gl);
-                    const int64_t f = fbase + r_next + w;
-                    const uint32_t src =
-                        __ldcg(ps.queue + static_cast<uint64_t>(f % ps.Q) * ps.n + s_lo[a] + (gl - seg[a]));
-                    if (w >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src;
-                    const uint32_t* sp = ps.split + static_cast<uint64_t>(src) * (C + 1) + c;
-                    sb = __ldg(sp);
-                    se = __ldg(sp + 1);
-                    my_deliv += se - sb;
-                    row4 = src * pitch4;
-                    base = (((r_next + w) % R) * ps.K + static_cast<uint32_t>(source_class(ps, src))) * ps.win_cap;
-                    nchunk = se > sb ? ((se + 3) >> 2) - (sb >> 2) : 0;
-                }
-                uint32_t total;
-                const uint32_t first = group_exclusive_scan<DT, UW, BAR_D>(nchunk, s_dtmp, total);
-                if (profiling) mark(P_GATHER);
-                for (uint32_t i0 = 0; i0 < total; i0 += cap) {
-                    // chunk list: {16-byte chunk index, ring base << 5 | hi << 2 | lo}
-                    for (uint32_t q = 0; q < nchunk; ++q) {
-                        const uint32_t it = first + q;
-                        if (it < i0 || it >= i0 + cap) continue;
-                        const uint32_t w0 = ((sb >> 2) + q) << 2;  // first word of the chunk
-                        const uint32_t lo = sb > w0 ? sb - w0 : 0;
-                        const uint32_t hi = min(4u, se - w0);
-                        chunks[it - i0] = make_uint2(row4 + (sb >> 2) + q, (base << 5) | (hi << 2) | lo);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t it = i0 + u * DT;
+                            if (it < items) {
+                                const uint32_t g = it / WQ, q = it - g * WQ;
+                                sw[g * WQ + (q ^ ((g >> swz_sh) & swz_m))] = v[u];
+                            }
+                        }
                     }
                     named_bar(BAR_D, DT);
                     if (profiling) mark(11);
-                    const uint32_t m = min(cap, total - i0);
-                    for (uint32_t k0 = dtid; k0 < m; k0 += kChunkBatch * DT) {
-                        uint2 d[kChunkBatch];
-                        uint4 x[kChunkBatch];
-#pragma unroll
-                        for (int u = 0; u < kChunkBatch; ++u) {
-                            const uint32_t k = k0 + u * DT;
-                            d[u] = k < m ? chunks[k] : make_uint2(0, 0);
+                    // (3) count: task = (16-byte column q, block of 32 spikes)
+                    const uint32_t nblk = (n + 31) / 32;
+                    for (uint32_t t = dwarp; t < WQ * nblk; t += DW) {
+                        const uint32_t blk = t / WQ, q = t - blk * WQ;
+                        const uint32_t g = blk * 32 + lane;
+                        const bool valid = g < n;
+                        uint4 x = make_uint4(0, 0, 0, 0);
+                        uint32_t grp = 0xffu;
+                        if (valid) {
+                            x = sw[g * WQ + (q ^ ((g >> swz_sh) & swz_m))];
+                            grp = s_grp[g];
                         }
-#pragma unroll
-                        for (int u = 0; u < kChunkBatch; ++u)
-                            x[u] = d[u].y ? ldg_stream4(cells4 + d[u].x) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-                        for (int u = 0; u < kChunkBatch; ++u) {
-                            const uint32_t lo = d[u].y & 3u, hi = (d[u].y >> 2) & 7u;
-                            uint32_t* cb = ring + (d[u].y >> 5) - alo;
-                            if (lo == 0 && hi > 0) atomicAdd(cb + x[u].x, 1u);
-                            if (lo <= 1 && hi > 1) atomicAdd(cb + x[u].y, 1u);
-                            if (lo <= 2 && hi > 2) atomicAdd(cb + x[u].z, 1u);
-                            if (hi > 3) atomicAdd(cb + x[u].w, 1u);
+                        x.x = transpose32(x.x, lane);
+                        x.y = transpose32(x.y, lane);
+                        x.z = transpose32(x.z, lane);
+                        x.w = transpose32(x.w, lane);
+                        unsigned rem = __ballot_sync(0xffffffffu, valid);
+                        while (rem) {
+                            const uint32_t G = __shfl_sync(0xffffffffu, grp, __ffs(rem) - 1);
+                            const unsigned gm = __ballot_sync(0xffffffffu, grp == G);
+                            rem &= ~gm;
+                            uint32_t* cb = ring + (((r_next + (G >> 2)) % R) * ps.K + (G & 3u)) * ps.win_cap +
+                                           q * 128 + lane;
+                            const uint32_t c0 = __popc(x.x & gm), c1 = __popc(x.y & gm);
+                            const uint32_t c2 = __popc(x.z & gm), c3 = __popc(x.w & gm);
+                            if (c0) atomicAdd(cb, c0);
+                            if (c1) atomicAdd(cb + 32, c1);
+                            if (c2) atomicAdd(cb + 64, c2);
+                            if (c3) atomicAdd(cb + 96, c3);
+                            my_deliv += c0 + c1 + c2 + c3;
                         }
                     }
-                    named_bar(BAR_D, DT);
+                    named_bar(BAR_D, DT);  // counts complete, staging reusable
+                    if (profiling) mark(P_DELIVER);
                 }
-                if (profiling) mark(P_DELIVER);
+            } else {
+                for (uint32_t g0 = 0; g0 < S; g0 += DT) {
+                    // one spike per thread: id, this CTA's row window, chunk count
+                    const uint32_t g = g0 + dtid;
+                    uint32_t nchunk = 0, sb = 0, se = 0, base = 0, row4 = 0;
+                    if (g < S) {
+                        uint32_t w = 0, fw = 0;
+    #pragma unroll
+                        for (int q = 1; q < kPipeMaxBatch; ++q)
+                            if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
+                                w = q;
+                                fw = fpre[q];
+                            }
+                        const uint32_t gl = g - fw;
+                        const uint32_t* seg = s_seg[w];
+                        const uint32_t a = piece_of(seg, P, gl);
+                        const int64_t f = fbase + r_next + w;
+                        const uint32_t src =
+                            __ldcg(ps.queue + static_cast<uint64_t>(f % ps.Q) * ps.n + s_lo[a] + (gl - seg[a]));
+                        if (w >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src;
+                        const uint32_t* sp = ps.split + static_cast<uint64_t>(src) * (C + 1) + c;
+                        sb = __ldg(sp);
+                        se = __ldg(sp + 1);
+                        my_deliv += se - sb;
+                        row4 = src * pitch4;
+                        base = (((r_next + w) % R) * ps.K + static_cast<uint32_t>(source_class(ps, src))) * ps.win_cap;
+                        nchunk = se > sb ? ((se + 3) >> 2) - (sb >> 2) : 0;
+                    }
+                    uint32_t total;
+                    const uint32_t first = group_exclusive_scan<DT, UW, BAR_D>(nchunk, s_dtmp, total);
+                    if (profiling) mark(P_GATHER);
+                    for (uint32_t i0 = 0; i0 < total; i0 += cap) {
+                        // chunk list: {16-byte chunk index, ring base << 5 | hi << 2 | lo}
+                        for (uint32_t q = 0; q < nchunk; ++q) {
+                            const uint32_t it = first + q;
+                            if (it < i0 || it >= i0 + cap) continue;
+                            const uint32_t w0 = ((sb >> 2) + q) << 2;  // first word of the chunk
+                            const uint32_t lo = sb > w0 ? sb - w0 : 0;
+                            const uint32_t hi = min(4u, se - w0);
+                            chunks[it - i0] = make_uint2(row4 + (sb >> 2) + q, (base << 5) | (hi << 2) | lo);
+                        }
+                        named_bar(BAR_D, DT);
+                        if (profiling) mark(11);
+                        const uint32_t m = min(cap, total - i0);
+                        for (uint32_t k0 = dtid; k0 < m; k0 += kChunkBatch * DT) {
+                            uint2 d[kChunkBatch];
+                            uint4 x[kChunkBatch];
+    #pragma unroll
+                            for (int u = 0; u < kChunkBatch; ++u) {
+                                const uint32_t k = k0 + u * DT;
+                                d[u] = k < m ? chunks[k] : make_uint2(0, 0);
+                            }
+    #pragma unroll
+                            for (int u = 0; u < kChunkBatch; ++u)
+                                x[u] = d[u].y ? ldg_stream4(cells4 + d[u].x) : make_uint4(0, 0, 0, 0);
+    #pragma unroll
+                            for (int u = 0; u < kChunkBatch; ++u) {
+                                const uint32_t lo = d[u].y & 3u, hi = (d[u].y >> 2) & 7u;
+                                uint32_t* cb = ring + (d[u].y >> 5) - alo;
+                                if (lo == 0 && hi > 0) atomicAdd(cb + x[u].x, 1u);
+                                if (lo <= 1 && hi > 1) atomicAdd(cb + x[u].y, 1u);
+                                if (lo <= 2 && hi > 2) atomicAdd(cb + x[u].z, 1u);
+                                if (hi > 3) atomicAdd(cb + x[u].w, 1u);
+                            }
+                        }
+                        named_bar(BAR_D, DT);
+                    }
+                    if (profiling) mark(P_DELIVER);
+                }
             }
             if (wlog < B) lc = lbase + S;
             // every counting atomic of the pass precedes the release (barrier)

@@ -659,7 +659,7 @@ private:
         SYNQ_CUDA(cudaGetDevice(&dev));
         SYNQ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         size_t smem = 0;
-        if (!setup_pipeline(K, wcap, longest, delay_, size_t(max_smem), smem)) {
+        if (!setup_pipeline(K, wcap, longest, delay_, size_t(max_smem), smem, alo)) {
             if (longest > max_local) return;
             // dynamic smem: counts only (delivery items are static)
             const size_t static_smem = 3 * (dev::kMaxPieces + 1) * 4 + 8192;
@@ -785,9 +785,10 @@ private:
     // fits: UW update warps hold <= 8 neurons per thread in registers; shared
     // memory holds a count ring of R <= delay frames, the row prefetch windows
     // and the chunk list.  Sets pipe_* and stage_items_; false = serial kernel.
-    bool setup_pipeline(int K, uint32_t wcap, uint32_t longest, uint32_t delay, size_t max_smem, size_t& smem)
-        requires population_model {
+    bool setup_pipeline(int K, uint32_t wcap, uint32_t longest, uint32_t delay, size_t max_smem, size_t& smem,
+                        const std::vector<uint32_t>& alo) requires population_model {
         pipe_ = false;
+        pipe_bm_ = false;
         int mode = opt_.pipeline;
         if (const char* e = std::getenv("SYNQ_PIPELINE")) mode = std::atoi(e);
         if (mode == 0) return false;
@@ -796,7 +797,7 @@ private:
         if (const char* e = std::getenv("SYNQ_UW")) uw_pref = std::atoi(e) == 8 ? 8 : 4;
         if (uw_pref == 8 && longest <= 8 * 32 * 8) {
             pipe_uw_ = 8;
-            pipe_npt_ = longest <= 256 ? 1 : (longest <= 512 ? 2 : (longest <= 1024 ? 4 : 8));
+            pipe_npt_ = longest <= 1024 ? 4 : 8;
         } else if (longest <= 4 * 32 * 8) {
             pipe_uw_ = 4;
             pipe_npt_ = longest <= 128 ? 1 : (longest <= 256 ? 2 : (longest <= 512 ? 4 : 8));
@@ -807,15 +808,27 @@ private:
             return false;
         }
         pipe_ = true;
+        // bitmap delivery when the receive-window bitmaps are clearly smaller
+        // than the ELL rows (dense connectivity, e.g. Brunel p = 0.1)
+        const uint32_t C = static_cast<uint32_t>(alo.size()) - 1;
+        uint32_t wq = (wcap + 127) / 128;
+        wq = wq <= 1 ? 1 : (wq <= 2 ? 2 : (wq <= 4 ? 4 : 8));
+        const uint64_t bm_bytes = uint64_t(n_) * C * wq * 16, ell_bytes = uint64_t(n_) * graph_.pitch * 4;
+        bool use_bm = wcap <= 1024 && 3 * bm_bytes < 2 * ell_bytes && K <= 4;
+        if (const char* e = std::getenv("SYNQ_BITMAP")) use_bm = use_bm && std::atoi(e) != 0;
+        pipe_bm_ = use_bm;
         cudaFuncAttributes attr{};
         SYNQ_CUDA(cudaFuncGetAttributes(&attr, kernel_fn()));
         const size_t avail = max_smem > attr.sharedSizeBytes ? max_smem - attr.sharedSizeBytes : 0;
         // L2 row prefetch pays once the adjacency outgrows L2
         bool prefetch = graph_.pitch * 4ull * n_ > (64ull << 20);
         if (const char* e = std::getenv("SYNQ_PREFETCH")) prefetch = std::atoi(e) != 0;
-        const uint32_t pf_cap = prefetch ? ((longest + 1) & ~1u) : 0;
+        const uint32_t pf_cap = prefetch && !use_bm ? ((longest + 1) & ~1u) : 0;
         const size_t slot_bytes = size_t(K) * wcap * 4;
-        const size_t fixed = size_t(pf_cap) * 8 + 2048 * 8 + 16;  // prefetch windows + a minimal chunk list
+        // bitmap: staged windows + id + group per spike; ELL: 8-byte chunk descriptors
+        const size_t item_bytes = use_bm ? size_t(wq) * 16 + 5 : 8;
+        const size_t min_items = use_bm ? 1024 : 2048;
+        const size_t fixed = size_t(pf_cap) * 8 + min_items * item_bytes + 16;
         if (avail <= fixed || slot_bytes == 0) {
             pipe_ = false;
             return false;
@@ -835,8 +848,16 @@ private:
         if (const char* e = std::getenv("SYNQ_LEAD")) lead = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         lead = std::max(lead, lag + 1);
         const size_t ring_bytes = ((R * K * wcap + 3) & ~uint64_t(3)) * 4;
-        const size_t chunk_cap = std::min<size_t>(16384, (avail - ring_bytes - size_t(pf_cap) * 8) / 8);
-        smem = ring_bytes + size_t(pf_cap) * 8 + chunk_cap * 8;
+        size_t chunk_cap = std::min<size_t>(use_bm ? 4096 : 16384,
+                                            (avail - ring_bytes - size_t(pf_cap) * 8 - 16) / item_bytes);
+        if (use_bm) chunk_cap &= ~size_t(15);
+        smem = ring_bytes + size_t(pf_cap) * 8 + chunk_cap * item_bytes + 16;
+        if (use_bm) {
+            std::vector<uint32_t> wlo(alo.begin(), alo.end() - 1), whi(alo.begin() + 1, alo.end());
+            build_window_bitmaps(graph_, wlo, whi, wq, bm_, stream_);
+            bm_wq_ = wq;
+            bm_row4_ = C * wq;
+        }
         stage_items_ = static_cast<uint32_t>(chunk_cap);
         ring_R_ = static_cast<uint32_t>(R);
         lead_ = std::max<uint32_t>(1, std::min(lead, delay));
@@ -845,23 +866,22 @@ private:
         return true;
     }
 
-    const void* kernel_fn() const requires population_model {
-        if (pipe_) {
-            if (pipe_uw_ == 8) {
-                switch (pipe_npt_) {
-                    case 1: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 1>);
-                    case 2: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 2>);
-                    case 4: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 4>);
-                    default: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 8>);
-                }
-            }
-            switch (pipe_npt_) {
-                case 1: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 1>);
-                case 2: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 2>);
-                case 4: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 4>);
-                default: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 8>);
-            }
+    template <bool BM>
+    static const void* pipeline_fn(uint32_t uw, uint32_t npt) requires population_model {
+        if (uw == 8) {
+            if (npt <= 4) return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 4, BM>);
+            return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 8, BM>);
         }
+        switch (npt) {
+            case 1: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 1, BM>);
+            case 2: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 2, BM>);
+            case 4: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 4, BM>);
+            default: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 8, BM>);
+        }
+    }
+
+    const void* kernel_fn() const requires population_model {
+        if (pipe_) return pipe_bm_ ? pipeline_fn<true>(pipe_uw_, pipe_npt_) : pipeline_fn<false>(pipe_uw_, pipe_npt_);
         return persistent_fn();
     }
 
@@ -912,6 +932,10 @@ private:
         p.lead = lead_;
         p.pf_cap = pf_cap_;
         p.lag = lag_;
+        p.bm = pipe_bm_ ? bm_.get() : nullptr;
+        p.bm_row4 = bm_row4_;
+        p.wq = bm_wq_;
+        p.bm_prefetch = pipe_bm_ && lag_ > 0 ? 1u : 0u;
         return p;
     }
 
@@ -1174,6 +1198,9 @@ private:
     uint32_t last_batch_b_ = 0;
     int npt_select_ = 1;
     bool pipe_ = false;  // pipelined kernel (detail/pipeline.cuh)
+    bool pipe_bm_ = false;  // ... with bitmap delivery
+    dev_array<uint4> bm_;
+    uint32_t bm_wq_ = 0, bm_row4_ = 0;
     uint32_t pipe_uw_ = 4, pipe_npt_ = 1, ring_R_ = 0, lead_ = 0, lag_ = 0, pf_cap_ = 0;
     size_t smem_ = 0;
     int npt_ = 1;

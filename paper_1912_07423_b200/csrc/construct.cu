@@ -377,6 +377,63 @@ void build_splits(const device_graph& g, const std::vector<uint32_t>& tile_lo,
     SYNQ_CUDA(cudaStreamSynchronize(stream));
 }
 
+// Receive-window bitmaps (pipeline.cuh, bitmap delivery): row s holds, for
+// every local CTA c, wq uint4 (= 128 * wq bits) whose bit k is set iff
+// target window_lo[c] + k is in row s.  One CTA assembles a row in shared
+// memory (targets arrive sorted, so neighbouring threads hit neighbouring
+// words) and writes it out with 16-byte stores.
+__global__ void k_window_bitmaps(const uint32_t* __restrict__ cells, const uint32_t* __restrict__ degree,
+                                 uint32_t neurons, uint32_t pitch, const uint32_t* __restrict__ tpos,
+                                 uint32_t row_words, uint4* __restrict__ bm) {
+    extern __shared__ __align__(16) uint32_t row[];
+    for (uint32_t s = blockIdx.x; s < neurons; s += gridDim.x) {
+        for (uint32_t w = threadIdx.x; w < row_words; w += blockDim.x) row[w] = 0;
+        __syncthreads();
+        const uint32_t d = degree[s];
+        const uint32_t* r = cells + static_cast<uint64_t>(s) * pitch;
+        for (uint32_t k = threadIdx.x; k < d; k += blockDim.x) {
+            const uint32_t e = __ldg(tpos + __ldg(r + k));
+            if (e != 0xffffffffu) atomicOr(&row[e >> 5], 1u << (e & 31));
+        }
+        __syncthreads();
+        uint4* out = bm + static_cast<uint64_t>(s) * (row_words / 4);
+        const uint4* rw = reinterpret_cast<const uint4*>(row);
+        for (uint32_t q = threadIdx.x; q < row_words / 4; q += blockDim.x) out[q] = rw[q];
+        __syncthreads();
+    }
+}
+
+void build_window_bitmaps(const device_graph& g, const std::vector<uint32_t>& window_lo,
+                          const std::vector<uint32_t>& window_hi, uint32_t wq, dev_array<uint4>& bm,
+                          cudaStream_t stream) {
+    const uint32_t C = static_cast<uint32_t>(window_lo.size());
+    const uint32_t row_words = C * wq * 4;
+    std::vector<uint32_t> tpos(std::max<uint32_t>(1, g.neurons), 0xffffffffu);
+    for (uint32_t c = 0; c < C; ++c)
+        for (uint32_t t = window_lo[c]; t < window_hi[c]; ++t) {
+            const uint32_t k = t - window_lo[c];
+            if (k >= wq * 128) throw std::invalid_argument("window bitmap: window wider than its row slice");
+            tpos[t] = (c * wq * 4 + k / 32) << 5 | (k % 32);
+        }
+    dev_array<uint32_t> dpos(tpos.size());
+    dpos.upload(tpos.data(), tpos.size(), stream);
+    bm.resize(std::max<size_t>(1, static_cast<size_t>(g.neurons) * (row_words / 4)));
+    if (g.neurons && row_words) {
+        const size_t smem = size_t(row_words) * 4;
+        if (smem > 48 * 1024)
+            SYNQ_CUDA(cudaFuncSetAttribute(k_window_bitmaps, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+        int sms = 0, dev = 0;
+        SYNQ_CUDA(cudaGetDevice(&dev));
+        SYNQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const uint32_t grid = std::min<uint32_t>(g.neurons, static_cast<uint32_t>(sms) * 8);
+        k_window_bitmaps<<<grid, 256, smem, stream>>>(g.cells.get(), g.degree.get(), g.neurons, g.pitch,
+                                                      dpos.get(), row_words, bm.get());
+        SYNQ_CUDA(cudaGetLastError());
+    }
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+}
+
 adjacency_list expand_jobs(const construction_plan& plan, uint32_t neurons, uint64_t seed,
                            thread_pool*) {
     device_graph g = expand_device_graph(plan, neurons, seed, nullptr);

@@ -18,13 +18,26 @@ steps = int(sys.argv[3]) if len(sys.argv) > 3 else 5000
 leads = [int(x) for x in sys.argv[4:]] or [2, 4, 8]
 prof = os.environ.get("SYNQ_PROFILE") == "1"
 
-variants = [("serial", 0, 0)] + [(f"pipe lead={L}", 1, L) for L in leads]
+# (name, pipeline mode, lead, environment for the engine setup)
+variants = [("serial", 0, 0, {})]
+for L in leads:
+    variants.append((f"ell lead={L}", 1, L, {"SYNQ_BITMAP": "0"}))
+    variants.append((f"bitmap lead={L}", 1, L, {"SYNQ_BITMAP": "1"}))
 if os.environ.get("AB_NO_SERIAL"):
     variants = variants[1:]
+if os.environ.get("AB_ONLY"):
+    variants = [v for v in variants if v[0].startswith(os.environ["AB_ONLY"])]
 ref = None
-for name, mode, lead in variants:
+for name, mode, lead, env in variants:
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     sim = synq.Sim(model, opts=synq.Opts(seed=1, deterministic=True, pipeline=mode, lead=lead, profile=prof),
                    synapses=int(syn))
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
     assert sim.pipelined == bool(mode), (name, sim.pipelined)
     sim.run(500)  # warm-up
     d0, k0 = sim.device_time()
