@@ -13,8 +13,8 @@ reference's `deliveries` (proj/include/synq/engine.hpp:408).
   library on its own stream around every run; max over ranks).
 * e2e: the same workload through the C ABI with spike recording on and the
   raster copied into host buffers each step (device->host bytes counted).
-* roofline: the persistent step kernel (update + receive fused) — algorithmic
-  bytes per launch / kernel time vs the measured HBM copy bandwidth.
+* roofline: the persistent step kernel (update + receive, warp-specialised) —
+  algorithmic bytes per launch / kernel time vs the measured HBM copy bandwidth.
 * cpu_baseline: the UNMODIFIED reference (oracle/_ref/libsynq_ref.so, built
   from /root/reference by oracle/Makefile) on a bounded sample of the same
   network, on this host's cores.
@@ -376,7 +376,7 @@ def main():
             "workload": "brunel_1e9" if args.synapses == 1e9 else "brunel",
             "synapses": sim.synapses, "neurons": n, "bio_s_per_step": 1.0, "dt_ms": 0.1,
             "delay_steps": sim.delay, "parallelism": f"dp{world} (replicas)" if world > 1 else "single",
-            "engine": "persistent target-tiled (exact)", "tiles": None,
+            "engine": f"{sim.engine} (exact)", "tiles": None,
             "l2": "inputs larger than L2 (adjacency %.2f GB)" % (sim.synapses * 4 / 1e9),
             "setup_s": round(setup_s, 2), "construction_fixups": sim.construction_fixups(),
         },
@@ -385,7 +385,8 @@ def main():
         "events_per_bio_s": events / args.steps / world,
         "roofline": {
             "bound": "hbm",
-            "kernel": "synq::dev::k_persistent<brunel_model> (update+receive fused)",
+            "kernel": ("synq::dev::k_pipeline<brunel_model, UW, NPT, bitmap> (warp-specialised update + receive)"
+                       if sim.engine == "pipelined-bitmap" else f"synq::dev step kernel ({sim.engine})"),
             "achieved": achieved,
             "peak": peak,
             "unit": "GB/s",
@@ -393,6 +394,9 @@ def main():
             "traffic": (traffic_step * per_launch_steps) if traffic_step else None,
             "traffic_source": traffic_src,
             "alg_bytes_per_launch": alg / world / max(1, launches),
+            "alg_bytes_definition": "SURVEY.md 8(d): 4 B per delivery (u32 target id) + 24 B per LIF and "
+                                    "32 B per Poisson neuron-step + 4 B per spike; the bitmap receive "
+                                    "format moves ~1.3 B per delivery of it",
             "receive_only_GBps": 4.0 * events / world / kern / 1e9 if kern > 0 else 0.0,
             "kernel_s": kern,
             "peak_source": peak_src,

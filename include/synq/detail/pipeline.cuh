@@ -70,7 +70,7 @@ SYNQ_DEV void named_bar(uint32_t id, uint32_t count) {
 }
 // wait until *p >= want (every calling thread acquires)
 SYNQ_DEV void wait_at_least(const uint32_t* p, uint32_t want) {
-    while (ld_acquire_cta(p) < want) __nanosleep(32);
+    while (ld_acquire_cta(p) < want) __nanosleep(64);
 }
 
 // exclusive scan of one value per thread over a named-barrier group of NTH
@@ -128,12 +128,12 @@ SYNQ_DEV uint32_t transpose32(uint32_t x, uint32_t lane) {
 // UW update warps (NPT neurons per update thread); the other warps deliver.
 // BM: bitmap delivery (receive-window bitmaps + transposed counting), else
 // 16-byte ELL row chunks counted with one shared-memory atomic per delivery.
-template <class M, int UW, int NPT, bool BM>
-__global__ void __launch_bounds__(kPipeThreads, 1)
+template <class M, int UW, int NPT, bool BM, int NT = kPipeThreads>
+__global__ void __launch_bounds__(NT, 1)
     k_pipeline(M model, persist_state<M> ps, int64_t t0, int32_t nsteps) {
     using NF = typename M::neuron_fields;
     constexpr size_t ACC = population_delivery<M>::acc_field;
-    constexpr int NT = kPipeThreads, NW = NT / 32;
+    constexpr int NW = NT / 32;
     constexpr int UT = UW * 32, DT = NT - UT, DW = NW - UW;
     constexpr uint32_t BAR_U = 1, BAR_D = 2;
     static_assert(DW >= kPipeMaxBatch, "one polling warp per frame of a pass");
@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
     __shared__ uint32_t s_seg[kPipeMaxBatch][kMaxPieces + 1];
     __shared__ unsigned long long s_fval[kPipeMaxBatch][kMaxTiles];
     __shared__ uint32_t s_ok[kPipeMaxBatch];
+    __shared__ uint32_t s_qbase[kPipeMaxBatch];  // queue slot base of frame w of the pass
+    __shared__ uint32_t s_cbase[kPipeMaxBatch];  // count-ring slot base of frame w of the pass
     __shared__ uint32_t s_dtmp[DW + 1];
     __shared__ uint32_t s_wa[NPT * UW], s_wb[NPT * UW], s_mw[UW], s_out[3];
     __shared__ uint32_t s_delivered;  // frames delivered: rel 0 .. s_delivered
@@ -203,13 +205,17 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
             if (j < na + nb) load_all(ps.nf, id_of(j), v[r]);
         }
         unsigned long long my_spikes = 0;
-        for (uint32_t s = 0; s < nrel; ++s) {
+        uint32_t slot = static_cast<uint32_t>(t0 % ps.Q);
+        for (uint32_t s = 0; s < nrel; ++s, slot = slot + 1 == ps.Q ? 0u : slot + 1) {
             const int64_t t = t0 + s;
-            const uint32_t slot = static_cast<uint32_t>(t % ps.Q);
             uint32_t* qslot = ps.queue + static_cast<uint64_t>(slot) * ps.n;
             // frames through rel s (needed) and s + delay - lead (pacing);
             // never beyond rel s + R - 1, whose ring slot this step frees
-            wait_at_least(&s_delivered, min(min(s + ps.delay - lead, s + R - 1), nrel));
+            // (one warp polls; the others wait on the hardware barrier, which
+            // costs no issue slots; the barrier orders the acquire before
+            // every update thread's ring reads)
+            if (warp == 0) wait_at_least(&s_delivered, min(min(s + ps.delay - lead, s + R - 1), nrel));
+            named_bar(BAR_U, UT);
             mark(P_POLL);
             uint32_t* cslot = ring + (s % R) * ps.K * ps.win_cap;
             bool spk[NPT];
@@ -241,13 +247,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
                     v[r] = vl;
                     rr[r] = rl;
                     live[r] = ll;
-                    mcount += (spk[r] && i >= ps.meas_lo && i < ps.meas_hi) ? 1u : 0u;
+                    if (spk[r] && i >= ps.meas_lo && i < ps.meas_hi) ++mcount;
                 }
-                const unsigned ba = __ballot_sync(0xffffffffu, spk[r] && j < na);
-                const unsigned bb = __ballot_sync(0xffffffffu, spk[r] && j >= na);
+                // lanes of this (warp, r) in the A piece: a lane prefix
+                const int na_here = static_cast<int>(na) - static_cast<int>(warp * 32 + r * UT);
+                const unsigned amask = na_here >= 32 ? 0xffffffffu : (na_here <= 0 ? 0u : (1u << na_here) - 1u);
+                const unsigned bal = __ballot_sync(0xffffffffu, spk[r]);
                 if (lane == 0) {
-                    s_wa[r * UW + warp] = __popc(ba);
-                    s_wb[r * UW + warp] = __popc(bb);
+                    s_wa[r * UW + warp] = __popc(bal & amask);
+                    s_wb[r * UW + warp] = __popc(bal & ~amask);
                 }
             }
             for (int o = 16; o; o >>= 1) mcount += __shfl_xor_sync(0xffffffffu, mcount, o);
@@ -292,14 +300,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
 #pragma unroll
             for (int r = 0; r < NPT; ++r) {
                 const uint32_t j = tid + r * UT;
-                const unsigned ba = __ballot_sync(0xffffffffu, spk[r] && j < na);
-                const unsigned bb = __ballot_sync(0xffffffffu, spk[r] && j >= na);
+                const int na_here = static_cast<int>(na) - static_cast<int>(warp * 32 + r * UT);
+                const unsigned amask = na_here >= 32 ? 0xffffffffu : (na_here <= 0 ? 0u : (1u << na_here) - 1u);
+                const unsigned bal = __ballot_sync(0xffffffffu, spk[r]);
                 const unsigned below = (1u << lane) - 1u;
                 if (spk[r]) {
                     if (j < na)
-                        qslot[alo + s_wa[r * UW + warp] + __popc(ba & below)] = id_of(j);
+                        qslot[alo + s_wa[r * UW + warp] + __popc(bal & amask & below)] = id_of(j);
                     else
-                        qslot[blo + s_wb[r * UW + warp] + __popc(bb & below)] = id_of(j);
+                        qslot[blo + s_wb[r * UW + warp] + __popc(bal & ~amask & below)] = id_of(j);
                 }
             }
             const uint32_t outa = s_out[0], outb = s_out[1], meas = s_out[2];
@@ -397,7 +406,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
                            (ps.lag == 0 || frame_complete(ps, fbase + r + ps.lag, false, ps.C))) {
                     ok = frame_prefix(ps, fbase + r, s_seg[dwarp], s_fval[dwarp], s_psrc, true);
                 }
-                if (lane == 0) s_ok[dwarp] = ok ? 1u : 0u;
+                if (lane == 0) {
+                    s_ok[dwarp] = ok ? 1u : 0u;
+                    s_qbase[dwarp] = static_cast<uint32_t>((fbase + r) % ps.Q) * ps.n;
+                    s_cbase[dwarp] = (r % R) * ps.K * ps.win_cap;
+                }
             }
             named_bar(BAR_D, DT);
             if (profiling) mark(10);
@@ -428,7 +441,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
                 // the pass in shared memory, then count arrivals per (frame,
                 // class, target) with warp bit-transposes + popc: one counting
                 // atomic per 32 targets x 32 spikes instead of one per delivery.
-                const uint32_t WQ = ps.wq;
+                const uint32_t WQ = ps.wq, wq_sh = WQ == 1 ? 0u : (WQ == 2 ? 1u : (WQ == 4 ? 2u : 3u));
                 uint4* sw = reinterpret_cast<uint4*>(chunks);  // cap x WQ, 16-byte slots swizzled
                 uint32_t* s_src = reinterpret_cast<uint32_t*>(sw + cap * WQ);
                 uint8_t* s_grp = reinterpret_cast<uint8_t*>(s_src + cap);
@@ -437,81 +450,110 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
                 const uint4* bmw = ps.bm + static_cast<uint64_t>(c) * WQ;
                 for (uint32_t g0 = 0; g0 < S; g0 += cap) {
                     const uint32_t n = min(cap, S - g0);
-                    // (1) spike ids and (frame, class) groups
-                    for (uint32_t i = dtid; i < n; i += DT) {
-                        const uint32_t g = g0 + i;
-                        uint32_t w = 0, fw = 0;
-#pragma unroll
-                        for (int q = 1; q < kPipeMaxBatch; ++q)
-                            if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
-                                w = q;
-                                fw = fpre[q];
-                            }
-                        const uint32_t gl = g - fw;
-                        const uint32_t* seg = s_seg[w];
-                        const uint32_t a = piece_of(seg, P, gl);
-                        const int64_t f = fbase + r_next + w;
-                        const uint32_t src =
-                            __ldcg(ps.queue + static_cast<uint64_t>(f % ps.Q) * ps.n + s_lo[a] + (gl - seg[a]));
-                        if (w >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src;
-                        s_src[i] = src;
-                        s_grp[i] = static_cast<uint8_t>(w * 4 + static_cast<uint32_t>(source_class(ps, src)));
-                    }
-                    named_bar(BAR_D, DT);
-                    if (profiling) mark(P_GATHER);
-                    // (2) windows -> shared memory (4 loads in flight per thread)
-                    const uint32_t items = n * WQ;
-                    for (uint32_t i0 = dtid; i0 < items; i0 += 4 * DT) {
-                        uint4 v[4];
+                    // (1) spike ids and (frame, class) groups, 4 ids in flight per thread
+                    for (uint32_t i0 = dtid; i0 < n; i0 += 4 * DT) {
+                        uint32_t src[4], wv[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const uint32_t it = i0 + u * DT;
-                            if (it < items) {
-                                const uint32_t g = it / WQ, q = it - g * WQ;
-                                v[u] = ldg_stream4(bmw + static_cast<uint64_t>(s_src[g]) * ps.bm_row4 + q);
+                            const uint32_t i = i0 + u * DT;
+                            wv[u] = 0;
+                            src[u] = 0;
+                            if (i < n) {
+                                const uint32_t g = g0 + i;
+                                uint32_t w = 0, fw = 0;
+#pragma unroll
+                                for (int q = 1; q < kPipeMaxBatch; ++q)
+                                    if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
+                                        w = q;
+                                        fw = fpre[q];
+                                    }
+                                const uint32_t gl = g - fw;
+                                const uint32_t* seg = s_seg[w];
+                                const uint32_t a = piece_of(seg, P, gl);
+                                src[u] = __ldcg(ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
+                                wv[u] = w;
                             }
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
+                            const uint32_t i = i0 + u * DT;
+                            if (i < n) {
+                                const uint32_t g = g0 + i;
+                                if (wv[u] >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src[u];
+                                s_src[i] = src[u];
+                                s_grp[i] = static_cast<uint8_t>(wv[u] * 4 + static_cast<uint32_t>(source_class(ps, src[u])));
+                            }
+                        }
+                    }
+                    named_bar(BAR_D, DT);
+                    if (profiling) mark(P_GATHER);
+                    // (2) windows -> shared memory (8 loads in flight per thread)
+                    const uint32_t items = n * WQ;
+                    for (uint32_t i0 = dtid; i0 < items; i0 += 8 * DT) {
+                        uint4 v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
                             const uint32_t it = i0 + u * DT;
                             if (it < items) {
-                                const uint32_t g = it / WQ, q = it - g * WQ;
+                                const uint32_t g = it >> wq_sh, q = it & (WQ - 1);
+                                v[u] = ldg_stream4(bmw + static_cast<uint64_t>(s_src[g]) * ps.bm_row4 + q);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const uint32_t it = i0 + u * DT;
+                            if (it < items) {
+                                const uint32_t g = it >> wq_sh, q = it & (WQ - 1);
                                 sw[g * WQ + (q ^ ((g >> swz_sh) & swz_m))] = v[u];
                             }
                         }
                     }
                     named_bar(BAR_D, DT);
                     if (profiling) mark(11);
-                    // (3) count: task = (16-byte column q, block of 32 spikes)
-                    const uint32_t nblk = (n + 31) / 32;
-                    for (uint32_t t = dwarp; t < WQ * nblk; t += DW) {
-                        const uint32_t blk = t / WQ, q = t - blk * WQ;
-                        const uint32_t g = blk * 32 + lane;
-                        const bool valid = g < n;
-                        uint4 x = make_uint4(0, 0, 0, 0);
-                        uint32_t grp = 0xffu;
-                        if (valid) {
-                            x = sw[g * WQ + (q ^ ((g >> swz_sh) & swz_m))];
-                            grp = s_grp[g];
+                    // (3) count: task = (16-byte column q, block of 32 spikes); two
+                    // independent tasks per iteration
+                    const uint32_t nblk = (n + 31) / 32, ntask = WQ * nblk;
+                    for (uint32_t t0 = dwarp; t0 < ntask; t0 += 2 * DW) {
+                        uint4 x[2];
+                        uint32_t grp[2], qq[2];
+                        bool valid[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const uint32_t t = t0 + u * DW;
+                            const uint32_t blk = t >> wq_sh, q = t & (WQ - 1);
+                            const uint32_t g = blk * 32 + lane;
+                            qq[u] = q;
+                            valid[u] = t < ntask && g < n;
+                            x[u] = make_uint4(0, 0, 0, 0);
+                            grp[u] = 0xffu;
+                            if (valid[u]) {
+                                x[u] = sw[g * WQ + (q ^ ((g >> swz_sh) & swz_m))];
+                                grp[u] = s_grp[g];
+                            }
                         }
-                        x.x = transpose32(x.x, lane);
-                        x.y = transpose32(x.y, lane);
-                        x.z = transpose32(x.z, lane);
-                        x.w = transpose32(x.w, lane);
-                        unsigned rem = __ballot_sync(0xffffffffu, valid);
-                        while (rem) {
-                            const uint32_t G = __shfl_sync(0xffffffffu, grp, __ffs(rem) - 1);
-                            const unsigned gm = __ballot_sync(0xffffffffu, grp == G);
-                            rem &= ~gm;
-                            uint32_t* cb = ring + (((r_next + (G >> 2)) % R) * ps.K + (G & 3u)) * ps.win_cap +
-                                           q * 128 + lane;
-                            const uint32_t c0 = __popc(x.x & gm), c1 = __popc(x.y & gm);
-                            const uint32_t c2 = __popc(x.z & gm), c3 = __popc(x.w & gm);
-                            if (c0) atomicAdd(cb, c0);
-                            if (c1) atomicAdd(cb + 32, c1);
-                            if (c2) atomicAdd(cb + 64, c2);
-                            if (c3) atomicAdd(cb + 96, c3);
-                            my_deliv += c0 + c1 + c2 + c3;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            x[u].x = transpose32(x[u].x, lane);
+                            x[u].y = transpose32(x[u].y, lane);
+                            x[u].z = transpose32(x[u].z, lane);
+                            x[u].w = transpose32(x[u].w, lane);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            unsigned rem = __ballot_sync(0xffffffffu, valid[u]);
+                            while (rem) {
+                                const uint32_t G = __shfl_sync(0xffffffffu, grp[u], __ffs(rem) - 1);
+                                const unsigned gm = __ballot_sync(0xffffffffu, grp[u] == G);
+                                rem &= ~gm;
+                                uint32_t* cb = ring + s_cbase[G >> 2] + (G & 3u) * ps.win_cap + qq[u] * 128 + lane;
+                                const uint32_t c0 = __popc(x[u].x & gm), c1 = __popc(x[u].y & gm);
+                                const uint32_t c2 = __popc(x[u].z & gm), c3 = __popc(x[u].w & gm);
+                                if (c0) atomicAdd(cb, c0);
+                                if (c1) atomicAdd(cb + 32, c1);
+                                if (c2) atomicAdd(cb + 64, c2);
+                                if (c3) atomicAdd(cb + 96, c3);
+                                my_deliv += c0 + c1 + c2 + c3;
+                            }
                         }
                     }
                     named_bar(BAR_D, DT);  // counts complete, staging reusable
@@ -533,16 +575,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1)
                         const uint32_t gl = g - fw;
                         const uint32_t* seg = s_seg[w];
                         const uint32_t a = piece_of(seg, P, gl);
-                        const int64_t f = fbase + r_next + w;
-                        const uint32_t src =
-                            __ldcg(ps.queue + static_cast<uint64_t>(f % ps.Q) * ps.n + s_lo[a] + (gl - seg[a]));
+                        const uint32_t src = __ldcg(ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
                         if (w >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src;
                         const uint32_t* sp = ps.split + static_cast<uint64_t>(src) * (C + 1) + c;
                         sb = __ldg(sp);
                         se = __ldg(sp + 1);
                         my_deliv += se - sb;
                         row4 = src * pitch4;
-                        base = (((r_next + w) % R) * ps.K + static_cast<uint32_t>(source_class(ps, src))) * ps.win_cap;
+                        base = s_cbase[w] + static_cast<uint32_t>(source_class(ps, src)) * ps.win_cap;
                         nchunk = se > sb ? ((se + 3) >> 2) - (sb >> 2) : 0;
                     }
                     uint32_t total;

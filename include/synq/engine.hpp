@@ -307,6 +307,7 @@ public:
     unsigned worker_count() const { return persistent_ ? tiles_ : static_cast<unsigned>(sms_); }
     bool persistent() const { return persistent_; }
     bool pipelined() const { return persistent_ && pipe_; }
+    bool bitmap_delivery() const { return persistent_ && pipe_ && pipe_bm_; }
     bool exact() const { return exact_ || persistent_; }
     uint64_t construction_fixups() const { return graph_.tie_fixups; }
     // device time of all run() calls (CUDA events on the engine stream) and of
@@ -680,7 +681,7 @@ private:
                                            max_smem - static_cast<int>(fa.sharedSizeBytes)));
         }
         int per_sm = 0;
-        SYNQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, dev::kPersistThreads, smem));
+        SYNQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(kernel_threads()), smem));
         if (per_sm < 1) return;
         if (opt_.profile) {
             prof_.resize(size_t(C) * dev::P_SLOTS);
@@ -793,9 +794,16 @@ private:
         if (const char* e = std::getenv("SYNQ_PIPELINE")) mode = std::atoi(e);
         if (mode == 0) return false;
         if (uint64_t(n_) * (graph_.pitch / 4) >= (1ull << 32)) return false;  // 32-bit chunk indices
-        uint32_t uw_pref = 4;
-        if (const char* e = std::getenv("SYNQ_UW")) uw_pref = std::atoi(e) == 8 ? 8 : 4;
-        if (uw_pref == 8 && longest <= 8 * 32 * 8) {
+        // update warps: 8 once a CTA holds more than 512 neurons (the update's
+        // per-thread chain is the critical path), else 4 (more deliverers)
+        uint32_t uw_pref = longest > 512 ? 8 : 4;
+        if (const char* e = std::getenv("SYNQ_UW")) uw_pref = static_cast<uint32_t>(std::atoi(e));
+        pipe_threads_ = dev::kPipeThreads;
+        if (uw_pref == 16 && longest <= 16 * 32 * 2) {  // 1024-thread CTAs: 16 update + 16 delivery warps
+            pipe_uw_ = 16;
+            pipe_npt_ = longest <= 512 ? 1 : 2;
+            pipe_threads_ = 1024;
+        } else if (uw_pref == 8 && longest <= 8 * 32 * 8) {
             pipe_uw_ = 8;
             pipe_npt_ = longest <= 1024 ? 4 : 8;
         } else if (longest <= 4 * 32 * 8) {
@@ -844,7 +852,9 @@ private:
         uint32_t lag = prefetch ? 1 : 0;
         if (const char* e = std::getenv("SYNQ_LAG")) lag = static_cast<uint32_t>(std::max(0, std::atoi(e)));
         lag = std::min(lag, delay - 1);
-        uint32_t lead = opt_.lead ? opt_.lead : lag + 4;
+        // lead: as far ahead as the queue ring allows (deliverers batch more
+        // frames per pass the further the update may run ahead)
+        uint32_t lead = opt_.lead ? opt_.lead : delay;
         if (const char* e = std::getenv("SYNQ_LEAD")) lead = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         lead = std::max(lead, lag + 1);
         const size_t ring_bytes = ((R * K * wcap + 3) & ~uint64_t(3)) * 4;
@@ -868,6 +878,10 @@ private:
 
     template <bool BM>
     static const void* pipeline_fn(uint32_t uw, uint32_t npt) requires population_model {
+        if (uw == 16) {
+            if (npt <= 1) return reinterpret_cast<const void*>(dev::k_pipeline<Model, 16, 1, BM, 1024>);
+            return reinterpret_cast<const void*>(dev::k_pipeline<Model, 16, 2, BM, 1024>);
+        }
         if (uw == 8) {
             if (npt <= 4) return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 4, BM>);
             return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 8, BM>);
@@ -879,6 +893,8 @@ private:
             default: return reinterpret_cast<const void*>(dev::k_pipeline<Model, 4, 8, BM>);
         }
     }
+
+    uint32_t kernel_threads() const { return pipe_ ? pipe_threads_ : static_cast<uint32_t>(dev::kPersistThreads); }
 
     const void* kernel_fn() const requires population_model {
         if (pipe_) return pipe_bm_ ? pipeline_fn<true>(pipe_uw_, pipe_npt_) : pipeline_fn<false>(pipe_uw_, pipe_npt_);
@@ -988,7 +1004,7 @@ private:
                 Model m = model_;
                 void* args[] = {&m, &ps, &t0, &nsteps};
                 SYNQ_CUDA(cudaLaunchCooperativeKernel(kernel_fn(), dim3(tiles_),
-                                                      dim3(dev::kPersistThreads), args, smem_, stream_));
+                                                      dim3(kernel_threads()), args, smem_, stream_));
                 launches_ += 1;
             }
         } else {
@@ -1202,6 +1218,7 @@ private:
     dev_array<uint4> bm_;
     uint32_t bm_wq_ = 0, bm_row4_ = 0;
     uint32_t pipe_uw_ = 4, pipe_npt_ = 1, ring_R_ = 0, lead_ = 0, lag_ = 0, pf_cap_ = 0;
+    uint32_t pipe_threads_ = dev::kPipeThreads;
     size_t smem_ = 0;
     int npt_ = 1;
     dev_array<unsigned long long> prof_;

@@ -274,7 +274,11 @@ class Sim:
 
     @property
     def pipelined(self) -> bool:
-        return lib().synq_sim_engine(self.h) == 2
+        return lib().synq_sim_engine(self.h) >= 2
+
+    @property
+    def engine(self) -> str:
+        return {0: "graph", 1: "persistent", 2: "pipelined", 3: "pipelined-bitmap"}[lib().synq_sim_engine(self.h)]
 
     @property
     def exact(self) -> bool:

@@ -61,6 +61,7 @@ public:
     virtual const spike_raster& raster() const = 0;
     virtual bool persistent() const = 0;
     virtual bool pipelined() const = 0;
+    virtual bool bitmap_delivery() const = 0;
     virtual bool exact() const = 0;
     virtual const std::vector<uint32_t>& step_spikes() const = 0;
     virtual void neuron_field_bytes(uint32_t f, void* out, uint64_t bytes) = 0;
@@ -188,6 +189,7 @@ public:
     const spike_raster& raster() const override { return raster_; }
     bool persistent() const override { return net_->persistent(); }
     bool pipelined() const override { return net_->pipelined(); }
+    bool bitmap_delivery() const override { return net_->bitmap_delivery(); }
     bool exact() const override { return net_->exact(); }
     const std::vector<uint32_t>& step_spikes() const override { return net_->step_spike_counts(); }
     void neuron_field_bytes(uint32_t f, void* out, uint64_t bytes) override {
@@ -260,7 +262,10 @@ void sim_base::write_stats(std::ostream& out) const {
             << "\n";
     } catch (const std::invalid_argument&) {
     }
-    out << "engine=" << (pipelined() ? "b200-pipelined" : (persistent() ? "b200-persistent" : "b200-graph")) << "\n"
+    out << "engine="
+        << (bitmap_delivery() ? "b200-pipelined-bitmap"
+                              : (pipelined() ? "b200-pipelined" : (persistent() ? "b200-persistent" : "b200-graph")))
+        << "\n"
         << "exact=" << (exact() ? 1 : 0) << "\n";
     out.flush();
 }
@@ -716,7 +721,7 @@ synq_status synq_sim_phase_cycles(const synq_sim* s, double out[15], uint32_t* t
 }
 int synq_sim_engine(const synq_sim* s) {
     if (!s || !s->impl->persistent()) return 0;
-    return s->impl->pipelined() ? 2 : 1;
+    return s->impl->bitmap_delivery() ? 3 : (s->impl->pipelined() ? 2 : 1);
 }
 int synq_sim_exact(const synq_sim* s) { return s && s->impl->exact() ? 1 : 0; }
 
