@@ -823,7 +823,11 @@ private:
         wq = wq <= 1 ? 1 : (wq <= 2 ? 2 : (wq <= 4 ? 4 : 8));
         const uint64_t bm_bytes = uint64_t(n_) * C * wq * 16, ell_bytes = uint64_t(n_) * graph_.pitch * 4;
         bool use_bm = wcap <= 1024 && 3 * bm_bytes < 2 * ell_bytes && K <= 4;
-        if (const char* e = std::getenv("SYNQ_BITMAP")) use_bm = use_bm && std::atoi(e) != 0;
+        // SYNQ_BITMAP: 0 = never, 1 = when smaller (default), 2 = whenever it fits
+        if (const char* e = std::getenv("SYNQ_BITMAP")) {
+            const int v = std::atoi(e);
+            use_bm = v == 0 ? false : (v == 2 ? (wcap <= 1024 && K <= 4) : use_bm);
+        }
         pipe_bm_ = use_bm;
         cudaFuncAttributes attr{};
         SYNQ_CUDA(cudaFuncGetAttributes(&attr, kernel_fn()));
