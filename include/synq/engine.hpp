@@ -182,6 +182,9 @@ public:
         if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
         for (auto& e : ev_)
             if (e) cudaEventDestroy(e);
+        for (auto& sl : slots_)
+            for (auto& e : sl.ev)
+                if (e) cudaEventDestroy(e);
         if (stream_) {
             cudaStreamSynchronize(stream_);
             cudaStreamDestroy(stream_);
@@ -200,6 +203,7 @@ public:
         step_spikes_host_.clear();
         expiring_host_.clear();
         logged_upto_ = 0;
+        log_pred_ = 0;
         std::fill(imported_upto_.begin(), imported_upto_.end(), 0);
         const int64_t zero = 0;
         SYNQ_CUDA(cudaMemcpyAsync(t_dev_.get(), &zero, sizeof zero, cudaMemcpyHostToDevice, stream_));
@@ -258,12 +262,31 @@ public:
         push_mirrors();
         auto t0 = clock::now();
         SYNQ_CUDA(cudaEventRecord(ev_[0], stream_));
-        while (steps > 0) {
-            const int64_t b = std::min<int64_t>(steps, batch_cap_);
-            run_batch(static_cast<uint32_t>(b));
-            steps -= b;
+        if (persistent_) {
+            // two batches in flight: batch k+1 is launched before the host
+            // emits batch k's frames (logs are written by the kernel straight
+            // into pinned host slots), so the GPU never idles on the host
+            int slot = 0;
+            bool pending = false;
+            while (steps > 0) {
+                const int64_t b = std::min<int64_t>(steps, batch_cap_);
+                launch_persistent(static_cast<uint32_t>(b), slot);
+                if (pending) finish_persistent(slot ^ 1);
+                pending = true;
+                slot ^= 1;
+                steps -= b;
+            }
+            if (pending) finish_persistent(slot ^ 1);
+            pull_counters();
+            if (flags_host_[1]) throw device_error("ordered delivery scratch overflow");
+            if (log_on_ && logged_upto_ < t_ && !sharded()) drain_log();
+        } else {
+            while (steps > 0) {
+                const int64_t b = std::min<int64_t>(steps, batch_cap_);
+                run_batch(static_cast<uint32_t>(b));
+                steps -= b;
+            }
         }
-        if (persistent_ && log_ids_ && logged_upto_ < t_ && !sharded()) drain_log();
         SYNQ_CUDA(cudaEventRecord(ev_[1], stream_));
         SYNQ_CUDA(cudaEventSynchronize(ev_[1]));
         float ms = 0;
@@ -414,6 +437,7 @@ public:
         if (tap_) {
             ensure_log();
             logged_upto_ = t_;  // a new tap observes frames from now on
+            log_pred_ = t_;
         } else {
             drop_log();
         }
@@ -540,9 +564,9 @@ private:
             det_ev_.resize(det_cap_);
         }
         batch_cap_ = opt_.batch_steps ? opt_.batch_steps : 1000;
-        step_spikes_dev_.resize(batch_cap_);
-        step_meas_dev_.resize(batch_cap_);
-        step_buf_.resize(2 * size_t(batch_cap_));
+        step_spikes_dev_.resize(2 * size_t(batch_cap_));
+        step_meas_dev_.resize(2 * size_t(batch_cap_));
+        step_buf_.resize(4 * size_t(batch_cap_));
     }
 
     // Partition for the persistent engine (detail/persistent.cuh): every CTA
@@ -716,21 +740,29 @@ private:
     }
 
     void drop_log() {
-        if (!log_ids_) return;
+        if (!log_on_) return;
         reset_graph();
         log_ids_ = dev_array<uint32_t>();
         log_cap_ = 0;
+        log_on_ = false;
     }
 
     void ensure_log() {
-        if (log_ids_) return;
+        if (log_on_) return;
         reset_graph();
+        log_on_ = true;
         // frames of one batch; the batch shrinks to keep the log bounded
         const uint64_t cap = std::max<uint64_t>(1024, std::min<uint64_t>(uint64_t(batch_cap_ + delay_) * n_, 1ull << 26));
-        log_ids_.resize(cap);
-        log_end_.resize(1);
         log_cap_ = cap;
-        log_host_.resize(cap);
+        if (persistent_) {
+            // written by the kernel in place (pinned, device-addressable)
+            plog_[0].resize(cap);
+            plog_[1].resize(cap);
+            plog_end_.resize(2);
+        } else {
+            log_ids_.resize(cap);
+            log_host_.resize(cap);
+        }
         // a persistent batch logs up to delay-1 frames of the previous batch too
         const uint64_t frames = cap / std::max<uint32_t>(1, n_);
         const uint64_t fit = frames > delay_ ? frames - delay_ : 1;
@@ -990,10 +1022,11 @@ private:
         cudaGraphDestroy(g);
     }
 
+    // one batch of the per-step kernel graph (generic engine), synchronous
     void run_batch(uint32_t b) {
         step_spikes_dev_.zero(stream_);
         step_meas_dev_.zero(stream_);
-        const bool logging = static_cast<bool>(log_ids_);
+        const bool logging = log_on_;
         if (logging && !persistent_) {
             const unsigned long long zero2[2] = {0, 0};
             SYNQ_CUDA(cudaMemcpyAsync(log_cursor_.get(), zero2, sizeof zero2, cudaMemcpyHostToDevice, stream_));
@@ -1062,50 +1095,119 @@ private:
         if (logging) {
             // generic: frames t_ .. t_end-1; persistent: frames logged_upto_ .. t_end-delay
             const int64_t last = persistent_ ? t_end - int64_t(delay_) : t_end - 1;
-            emit_logged(logged, last);
+            emit_logged(log_host_.data(), logged, last);
         }
         t_ = t_end;
+    }
+
+    // persistent engine: enqueue one batch into slot `slot` (kernel, step
+    // counts -> pinned host, completion event); t_ advances at launch
+    void launch_persistent(uint32_t b, int slot) {
+        if constexpr (population_model) {
+            auto ps = pstate();
+            ps.step_spikes = step_spikes_dev_.get() + size_t(slot) * batch_cap_;
+            ps.step_meas = step_meas_dev_.get() + size_t(slot) * batch_cap_;
+            batch_slot& fl = slots_[slot];
+            fl.t0 = t_;
+            fl.b = b;
+            fl.logging = log_on_;
+            if (log_on_) {
+                ps.log = plog_[slot].get();
+                ps.log_end = plog_end_.get() + slot;
+                ps.log_cap = log_cap_;
+                ps.log_from = log_pred_;
+                plog_end_[slot] = 0;
+                // frames logged_upto_ .. t_end-delay are emitted when it finishes
+                log_pred_ = std::max(log_pred_, t_ + int64_t(b) - int64_t(delay_) + 1);
+            } else {
+                ps.log = nullptr;
+            }
+            SYNQ_CUDA(cudaMemsetAsync(ps.step_spikes, 0, sizeof(uint32_t) * b, stream_));
+            SYNQ_CUDA(cudaMemsetAsync(ps.step_meas, 0, sizeof(uint32_t) * b, stream_));
+            if (!fl.ev[0])
+                for (auto& e : fl.ev) SYNQ_CUDA(cudaEventCreate(&e));
+            SYNQ_CUDA(cudaEventRecord(fl.ev[0], stream_));
+            int64_t t0 = t_;
+            int32_t nsteps = static_cast<int32_t>(b);
+            Model m = model_;
+            void* args[] = {&m, &ps, &t0, &nsteps};
+            SYNQ_CUDA(cudaLaunchCooperativeKernel(kernel_fn(), dim3(tiles_), dim3(kernel_threads()), args, smem_,
+                                                  stream_));
+            SYNQ_CUDA(cudaGetLastError());
+            launches_ += 1;
+            SYNQ_CUDA(cudaEventRecord(fl.ev[1], stream_));
+            uint32_t* hb = step_buf_.data() + size_t(slot) * 2 * batch_cap_;
+            SYNQ_CUDA(cudaMemcpyAsync(hb, ps.step_spikes, sizeof(uint32_t) * b, cudaMemcpyDeviceToHost, stream_));
+            SYNQ_CUDA(cudaMemcpyAsync(hb + b, ps.step_meas, sizeof(uint32_t) * b, cudaMemcpyDeviceToHost, stream_));
+            d2h_bytes_ += 8ull * b;
+            SYNQ_CUDA(cudaEventRecord(fl.ev[2], stream_));
+            t_ += b;
+        }
+    }
+
+    // wait for slot `slot`'s batch and do its host bookkeeping / emission
+    void finish_persistent(int slot) {
+        batch_slot& fl = slots_[slot];
+        SYNQ_CUDA(cudaEventSynchronize(fl.ev[2]));
+        float ms = 0;
+        SYNQ_CUDA(cudaEventElapsedTime(&ms, fl.ev[0], fl.ev[1]));
+        kernel_seconds_ += ms * 1e-3;
+        const uint32_t b = fl.b;
+        const uint32_t* hb = step_buf_.data() + size_t(slot) * 2 * batch_cap_;
+        // per-step bookkeeping, frames_consumed (engine.hpp:371-380)
+        for (uint32_t k = 0; k < b; ++k) {
+            step_spikes_host_.push_back(hb[k]);
+            step_measured_.push_back(hb[b + k]);
+            if (fl.t0 + k - int64_t(delay_) + 1 >= 0) ++counters_.frames_consumed;
+        }
+        counters_.steps += b;
+        if (fl.logging) {
+            const uint64_t end = plog_end_[slot];
+            if (end > log_cap_) throw device_error("spike log overflow (batch too large for the frame log)");
+            d2h_bytes_ += 8 + 4 * end;  // written to host memory by the kernel
+            emit_logged(plog_[slot].data(), end, fl.t0 + int64_t(b) - int64_t(delay_));
+        }
     }
 
     uint64_t kernels_per_step() const {
         return 2 + (has_synapses ? 1 : 0) + (exact_ ? 3 : 0);
     }
 
-    // frames logged_upto_ .. last are the next entries of log_host_, in order
-    void emit_logged(uint64_t logged, int64_t last) {
-        std::vector<uint32_t> frame;
+    // frames logged_upto_ .. last are the next entries of `log`, in order
+    void emit_logged(const uint32_t* log, uint64_t logged, int64_t last) {
         uint64_t off = 0;
         for (int64_t f = logged_upto_; f <= last; ++f) {
             const uint32_t cnt = step_spikes_host_[static_cast<size_t>(f)];
-            frame.assign(log_host_.data() + std::min(off, logged), log_host_.data() + std::min(off + cnt, logged));
+            const uint64_t a = std::min(off, logged), e = std::min(off + cnt, logged);
             off += cnt;
-            emit(f, frame);
+            emit(f, std::span<const uint32_t>(log + a, e - a));
         }
         logged_upto_ = std::max(logged_upto_, last + 1);
+        log_pred_ = std::max(log_pred_, logged_upto_);
     }
 
     void drain_log() {
         if constexpr (population_model) {
             auto ps = pstate();
+            ps.log = plog_[0].get();
+            ps.log_end = plog_end_.get();
+            ps.log_cap = log_cap_;
+            plog_end_[0] = 0;
             dev::k_log_drain<Model><<<1, 1024, 0, stream_>>>(ps, logged_upto_, t_ - 1);
             SYNQ_CUDA(cudaGetLastError());
             launches_ += 1;
-            unsigned long long end = 0;
-            SYNQ_CUDA(cudaMemcpyAsync(&end, log_end_.get(), sizeof end, cudaMemcpyDeviceToHost, stream_));
             SYNQ_CUDA(cudaStreamSynchronize(stream_));
-            const uint64_t logged = std::min<uint64_t>(end, log_cap_);
-            log_ids_.download(log_host_.data(), logged, stream_);
-            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            const uint64_t logged = std::min<uint64_t>(plog_end_[0], log_cap_);
             d2h_bytes_ += 8 + 4 * logged;
-            emit_logged(logged, t_ - 1);
+            emit_logged(plog_[0].data(), logged, t_ - 1);
         }
     }
 
-    void emit(int64_t t, const std::vector<uint32_t>& frame) {
+    void emit(int64_t t, std::span<const uint32_t> frame) {
         if (opt_.debug_checks)
             for (size_t i = 1; i < frame.size(); ++i)
                 if (frame[i - 1] >= frame[i]) throw std::logic_error("spike frame not sorted/unique");
-        if (tap_) tap_(t, std::span<const uint32_t>(frame.data(), frame.size()));
+        if (tap_) tap_(t, frame);
     }
 
     void pull_counters() {
@@ -1190,6 +1292,17 @@ private:
     dev_array<unsigned long long> log_end_;
     pinned_array<uint32_t> log_host_;
     int64_t logged_upto_ = 0;
+    int64_t log_pred_ = 0;  // first frame the next persistent launch logs
+    bool log_on_ = false;
+    pinned_array<uint32_t> plog_[2];          // persistent engine: frame logs, one per batch slot
+    pinned_array<unsigned long long> plog_end_;
+    struct batch_slot {
+        int64_t t0 = 0;
+        uint32_t b = 0;
+        bool logging = false;
+        cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // kernel start, kernel end, copies done
+    };
+    batch_slot slots_[2];
     cudaEvent_t ev_[4] = {nullptr, nullptr, nullptr, nullptr};
     double device_seconds_ = 0, kernel_seconds_ = 0;
     uint64_t launches_ = 0, h2d_bytes_ = 0, d2h_bytes_ = 0;

@@ -145,10 +145,13 @@ public:
     }
     void set_record(bool on) override {
         record_ = on;
-        raster_.records.clear();
+        raster_.records.clear();  // keeps its capacity: a recurring recording reuses the pages
         if (on)
             net_->set_spike_tap([this](int64_t t, std::span<const uint32_t> frame) {
-                for (uint32_t id : frame) raster_.records.push_back({t, id});
+                auto& r = raster_.records;
+                const size_t o = r.size(), n = frame.size();
+                if (r.capacity() < o + n) r.reserve(std::max<size_t>(2 * r.capacity(), o + n + (size_t(1) << 20)));
+                for (size_t k = 0; k < n; ++k) r.push_back({t, frame[k]});
             });
         else
             net_->set_spike_tap(nullptr);
