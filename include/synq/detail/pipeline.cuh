@@ -105,6 +105,16 @@ SYNQ_DEV uint32_t group_exclusive_scan(uint32_t x, uint32_t* s_tmp, uint32_t& to
     return r;
 }
 
+// Ampere-style asynchronous global->shared copies (LDGSTS): no registers
+// are held while the copies are in flight
+SYNQ_DEV void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+SYNQ_DEV void cp_async16_cg(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+SYNQ_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // 32x32 bit transpose across a warp: lane i holds row i on entry, lane b
 // holds column b on exit (bit i = bit b of lane i's entry word).  Stages 16
 // and 8 are byte permutes, stages 4 / 2 / 1 a rotate plus a masked merge.
@@ -450,64 +460,42 @@ __global__ void __launch_bounds__(NT, 1)
                 const uint4* bmw = ps.bm + static_cast<uint64_t>(c) * WQ;
                 for (uint32_t g0 = 0; g0 < S; g0 += cap) {
                     const uint32_t n = min(cap, S - g0);
-                    // (1) spike ids and (frame, class) groups, 4 ids in flight per thread
-                    for (uint32_t i0 = dtid; i0 < n; i0 += 4 * DT) {
-                        uint32_t src[4], wv[4];
+                    // (1) spike ids: every thread issues all its 4-byte
+                    // global->shared copies (cp.async, no registers held), then
+                    // one wait: a single latency round per pass
+                    for (uint32_t i = dtid; i < n; i += DT) {
+                        const uint32_t g = g0 + i;
+                        uint32_t w = 0, fw = 0;
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const uint32_t i = i0 + u * DT;
-                            wv[u] = 0;
-                            src[u] = 0;
-                            if (i < n) {
-                                const uint32_t g = g0 + i;
-                                uint32_t w = 0, fw = 0;
-#pragma unroll
-                                for (int q = 1; q < kPipeMaxBatch; ++q)
-                                    if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
-                                        w = q;
-                                        fw = fpre[q];
-                                    }
-                                const uint32_t gl = g - fw;
-                                const uint32_t* seg = s_seg[w];
-                                const uint32_t a = piece_of(seg, P, gl);
-                                src[u] = __ldcg(ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
-                                wv[u] = w;
+                        for (int q = 1; q < kPipeMaxBatch; ++q)
+                            if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
+                                w = q;
+                                fw = fpre[q];
                             }
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const uint32_t i = i0 + u * DT;
-                            if (i < n) {
-                                const uint32_t g = g0 + i;
-                                if (wv[u] >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src[u];
-                                s_src[i] = src[u];
-                                s_grp[i] = static_cast<uint8_t>(wv[u] * 4 + static_cast<uint32_t>(source_class(ps, src[u])));
-                            }
-                        }
+                        const uint32_t gl = g - fw;
+                        const uint32_t* seg = s_seg[w];
+                        const uint32_t a = piece_of(seg, P, gl);
+                        cp_async4(s_src + i, ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
+                        s_grp[i] = static_cast<uint8_t>(w);
                     }
+                    cp_async_wait_all();
                     named_bar(BAR_D, DT);
-                    if (profiling) mark(P_GATHER);
-                    // (2) windows -> shared memory (8 loads in flight per thread)
-                    const uint32_t items = n * WQ;
-                    for (uint32_t i0 = dtid; i0 < items; i0 += 8 * DT) {
-                        uint4 v[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const uint32_t it = i0 + u * DT;
-                            if (it < items) {
-                                const uint32_t g = it >> wq_sh, q = it & (WQ - 1);
-                                v[u] = ldg_stream4(bmw + static_cast<uint64_t>(s_src[g]) * ps.bm_row4 + q);
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const uint32_t it = i0 + u * DT;
-                            if (it < items) {
-                                const uint32_t g = it >> wq_sh, q = it & (WQ - 1);
-                                sw[g * WQ + (q ^ ((g >> swz_sh) & swz_m))] = v[u];
-                            }
-                        }
+                    // (frame, class) group of each spike; CTA 0 logs the frames
+                    for (uint32_t i = dtid; i < n; i += DT) {
+                        const uint32_t src = s_src[i], w = s_grp[i];
+                        if (w >= wlog && lbase + g0 + i < ps.log_cap) ps.log[lbase + g0 + i] = src;
+                        s_grp[i] = static_cast<uint8_t>(w * 4 + static_cast<uint32_t>(source_class(ps, src)));
                     }
+                    if (profiling) mark(P_GATHER);
+                    // (2) windows -> shared memory: 16-byte cp.async.cg copies,
+                    // all issued back to back, one wait
+                    const uint32_t items = n * WQ;
+                    for (uint32_t it = dtid; it < items; it += DT) {
+                        const uint32_t g = it >> wq_sh, q = it & (WQ - 1);
+                        cp_async16_cg(sw + g * WQ + (q ^ ((g >> swz_sh) & swz_m)),
+                                      bmw + static_cast<uint64_t>(s_src[g]) * ps.bm_row4 + q);
+                    }
+                    cp_async_wait_all();
                     named_bar(BAR_D, DT);
                     if (profiling) mark(11);
                     // (3) count: task = (16-byte column q, block of 32 spikes); two
