@@ -37,11 +37,11 @@ $(OBJDIR)/%.o: $(PKG)/csrc/%.cpp $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-LIB_OBJS := $(OBJDIR)/capi.o $(OBJDIR)/construct.o $(OBJDIR)/host_model.o
+LIB_OBJS := $(OBJDIR)/capi.o $(OBJDIR)/construct.o $(OBJDIR)/host_model.o $(OBJDIR)/nccl_glue.o
 
 $(LIBDIR)/libsynq.so.1: $(LIB_OBJS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -Xlinker -soname,libsynq.so.1 -o $@ $(LIB_OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -Xlinker -soname,libsynq.so.1 -o $@ $(LIB_OBJS) -lcudart -lnccl
 	ln -sf libsynq.so.1 $(LIBDIR)/libsynq.so
 
 oracle:

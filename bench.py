@@ -21,8 +21,10 @@ reference's `deliveries` (proj/include/synq/engine.hpp:408).
 * --impl reference: the reference's own CPU simulator on this host: deterministic
   (1 thread) and parallel (all threads) modes, the faster reported.
 Inputs are larger than L2 (4.2 GB adjacency vs 126 MB L2), so no L2 flush.
-Under torchrun (N > 1) every rank runs its own 1e9-synapse replica (weak
-scaling); rank 0 prints the JSON line.
+Under torchrun (N > 1) the ranks shard ONE network of N x 1e9 synapses
+(target-partitioned, spike frames allgathered over NCCL every delay-1 steps;
+weak scaling); `--replicas` runs independent 1e9-synapse replicas instead.
+Rank 0 prints the JSON line.
 """
 from __future__ import annotations
 
@@ -56,6 +58,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-steps", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent 1e9-synapse replicas instead of one sharded network")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 frame exchange (gloo: host buffers, e.g. several ranks on one GPU)")
     return ap.parse_args()
 
 
@@ -264,8 +270,10 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+        dist.init_process_group(args.backend)
+        if not args.replicas:
+            return run_sharded(args, rank, world, local)
     os.environ.setdefault("CUDA_DEVICE_ORDER", "PCI_BUS_ID")
     import paper_1912_07423_b200 as synq
 
@@ -434,6 +442,151 @@ def main():
             }
     print(json.dumps(line))
     sim.close()
+    return 0
+
+
+def run_sharded(args, rank, world, local):
+    """N>1: ONE Brunel network of N x `--synapses` synapses,
+    target-partitioned over the N GPUs (weak scaling: ~1e9 synapses and the
+    same deliveries per step per GPU).  Every rank updates its own neurons and
+    delivers every spike of the network onto its own targets; the spike
+    frames are exchanged with an allgather (NCCL over NVLink, device buffers)
+    every delay-1 steps, which is exact because a spike is due delay steps
+    after it fires."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_07423_b200 as synq
+    from paper_1912_07423_b200 import shard
+
+    total = int(args.synapses * world)
+    in_engine = args.backend == "nccl"
+    t_setup = time.perf_counter()
+    if in_engine:
+        # the engine allgathers the frames itself (ncclAllGather on its own
+        # stream after every batch): one NCCL id, broadcast from rank 0
+        uid = [synq.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sim = synq.Sim("brunel", opts=synq.Opts(seed=args.seed, deterministic=True,
+                                                shard_nccl=(rank, world, uid[0])), synapses=total)
+
+        class _Engine:  # the ShardedSim surface bench needs
+            record = False
+            frames: list = []
+
+            def run(self, steps):
+                sim.run(steps)
+
+            def close(self):
+                sim.close()
+
+        ss = _Engine()
+    else:
+        sim = synq.Sim("brunel", opts=synq.Opts(seed=args.seed, deterministic=True, shard=(rank, world)),
+                       synapses=total)
+        ss = shard.ShardedSim("brunel", 0, transport=shard.TorchTransport(), sim=sim)
+    setup_s = time.perf_counter() - t_setup
+    ss.run(args.warmup * BIO_STEPS)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    sync_all()
+    c0, l0 = sim.counters(), sim.kernel_launches()
+    _, ker0 = sim.device_time()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    with ClockSampler(local % max(1, torch.cuda.device_count())) as clocks:
+        ss.run(args.steps * BIO_STEPS)
+        torch.cuda.synchronize()
+    ev1.record()
+    ev1.synchronize()
+    secs = ev0.elapsed_time(ev1) * 1e-3
+    c1, l1 = sim.counters(), sim.kernel_launches()
+    _, ker1 = sim.device_time()
+    sync_all()
+
+    # e2e: the global spike raster on the host (in-engine: every rank's
+    # engine logs the merged frames into pinned memory and rank 0 copies the
+    # raster out through the C ABI; host path: frames merged from the gathered
+    # words), one untimed second first
+    if in_engine:
+        if rank == 0:
+            sim.set_record(True)
+        ss.run(BIO_STEPS)
+        if rank == 0:
+            sim.raster()
+            sim.set_record(True)
+    else:
+        ss.record = True
+        ss.run(BIO_STEPS)
+        ss.frames.clear()
+    sync_all()
+    e0 = sim.counters()["deliveries"]
+    h0, d0b = sim.transfer_bytes()
+    t0 = time.perf_counter()
+    gathered = 0
+    for _ in range(args.e2e_steps):
+        ss.run(BIO_STEPS)
+        if in_engine:
+            if rank == 0:
+                st, ids = sim.raster()
+                gathered += int(st.nbytes + ids.nbytes)
+                sim.set_record(True)
+        else:
+            gathered += sum(int(f.nbytes) for f in ss.frames)
+            ss.frames.clear()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if in_engine and rank == 0:
+        sim.set_record(False)
+    e2e_ev = sim.counters()["deliveries"] - e0
+    h1, d1b = sim.transfer_bytes()
+
+    dev = torch.device("cuda") if args.backend == "nccl" else torch.device("cpu")
+    mx = torch.tensor([secs, e2e_s, ker1 - ker0], dtype=torch.float64, device=dev)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = torch.tensor([c1["deliveries"] - c0["deliveries"], c1["spikes"] - c0["spikes"], e2e_ev, l1 - l0,
+                       (d1b - d0b) + gathered], dtype=torch.float64, device=dev)
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    secs, e2e_s, kern = (float(x) for x in mx.tolist())
+    events, spikes, e2e_events, launches, d2h = (float(x) for x in sm.tolist())
+    if rank != 0:
+        ss.close()
+        return 0
+    n = sim.neurons
+    n_exc = int(round(0.4 * n))
+    n_rec = n_exc + int(round(0.1 * n))
+    timesteps = args.steps * BIO_STEPS
+    alg = 4.0 * events + (24.0 * n_rec + 32.0 * (n - n_rec)) * timesteps + 4.0 * spikes
+    peak, peak_src = measured_peaks()
+    achieved = alg / world / kern / 1e9 if kern > 0 else 0.0
+    line = {
+        "metric": METRIC, "value": events / secs, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1000.0, "wall_s_per_bio_s": secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: Brunel network built on device from seed %d (reference RNG streams)" % args.seed,
+        "config": {"workload": f"brunel_{world}x1e9_sharded", "synapses": sim.synapses, "neurons": n,
+                   "bio_s_per_step": 1.0, "dt_ms": 0.1, "delay_steps": sim.delay,
+                   "parallelism": f"shard{world} (target-partitioned; " + (
+                       f"in-engine ncclAllGather of spike bitmasks every {sim.delay - 1} steps)" if in_engine else
+                       f"host-driven {args.backend} allgather of spike frames every {sim.delay - 1} steps)"),
+                   "engine": f"{sim.engine} shard (exact)", "setup_s": round(setup_s, 2),
+                   "l2": "inputs larger than L2"},
+        "gpu_launches": int(launches),
+        "spikes_per_bio_s": spikes / args.steps, "events_per_bio_s": events / args.steps,
+        "roofline": {"bound": "hbm", "kernel": f"synq::dev step kernel ({sim.engine}), per GPU",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel_s": kern, "peak_source": peak_src,
+                     "alg_bytes_definition": "SURVEY.md 8(d), whole network / N GPUs"},
+        "e2e": {"value": e2e_events / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0.0,
+                "d2h_bytes_per_step": d2h / max(1, args.e2e_steps + 1) / world,
+                "how": "sharded run; the global spike raster copied to host numpy buffers every bio-second"},
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line))
+    ss.close()
     return 0
 
 

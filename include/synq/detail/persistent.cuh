@@ -629,62 +629,209 @@ __global__ void k_log_drain(persist_state<M> ps, int64_t from, int64_t to) {
 //   words[0] = b, words[1 + 2k] / [2 + 2k] = A / B spike count of step k,
 //   then the ids of every step: A piece ids (CTA order) then B piece ids.
 // A and B pieces of one shard are contiguous id ranges, so a remote shard's
-// frame slice is two contiguous runs.
+// frame slice is two contiguous runs.  One warp per step; the lanes split the
+// C publishers (warp scans give every CTA's offset), so the exchange costs a
+// few L2 round trips per batch, not one per (step, CTA).
+
+// warp-wide inclusive scan
+SYNQ_DEV uint32_t warp_incl_scan(uint32_t x) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<uint32_t>(o)) x += y;
+    }
+    return x;
+}
+
 template <class M>
 __global__ void k_export(persist_state<M> ps, int64_t t0, uint32_t b, uint32_t* out) {
-    __shared__ uint32_t s_a[kMaxTiles + 1], s_b[kMaxTiles + 1], s_base;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t C = ps.C;
-    if (threadIdx.x == 0) {
-        out[0] = b;
-        s_base = 1 + 2 * b;
+    if (threadIdx.x == 0) out[0] = b;
+    // (1) per-step totals into the header
+    for (uint32_t k = warp; k < b; k += nw) {
+        const uint64_t* fi = reinterpret_cast<const uint64_t*>(ps.finfo) + static_cast<uint64_t>((t0 + k) % ps.Q) * ps.E;
+        uint32_t ta = 0, tb = 0;
+        for (uint32_t c = lane; c < C; c += 32) {
+            const unsigned long long e = fi[c];
+            ta += word_a(e);
+            tb += word_b(e);
+        }
+        for (int o = 16; o; o >>= 1) {
+            ta += __shfl_xor_sync(0xffffffffu, ta, o);
+            tb += __shfl_xor_sync(0xffffffffu, tb, o);
+        }
+        if (lane == 0) {
+            out[1 + 2 * k] = ta;
+            out[2 + 2 * k] = tb;
+        }
     }
-    for (uint32_t k = 0; k < b; ++k) {
+    __syncthreads();
+    // (2) per step: base offset from the header, then every CTA's slices
+    for (uint32_t k = warp; k < b; k += nw) {
+        uint32_t before = 0;
+        for (uint32_t q = lane; q < k; q += 32) before += out[1 + 2 * q] + out[2 + 2 * q];
+        for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+        const uint32_t base = 1 + 2 * b + before, ta = out[1 + 2 * k];
         const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t ra = 0, rb = 0;
-            for (uint32_t c = 0; c < C; ++c) {
-                const unsigned long long e = ps.finfo[static_cast<uint64_t>(slot) * ps.E + c];
-                s_a[c] = ra;
-                s_b[c] = rb;
-                ra += word_a(e);
-                rb += word_b(e);
-            }
-            s_a[C] = ra;
-            s_b[C] = rb;
-            out[1 + 2 * k] = ra;
-            out[2 + 2 * k] = rb;
-        }
-        __syncthreads();
-        const uint32_t base = s_base;
+        const uint64_t* fi = reinterpret_cast<const uint64_t*>(ps.finfo) + static_cast<uint64_t>(slot) * ps.E;
         const uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
-        for (uint32_t c = 0; c < C; ++c) {
-            const uint32_t alo = ps.piece_lo[ps.cta_piece[2 * c]], blo = ps.piece_lo[ps.cta_piece[2 * c + 1]];
-            for (uint32_t j = threadIdx.x; j < s_a[c + 1] - s_a[c]; j += blockDim.x) out[base + s_a[c] + j] = q[alo + j];
-            for (uint32_t j = threadIdx.x; j < s_b[c + 1] - s_b[c]; j += blockDim.x)
-                out[base + s_a[C] + s_b[c] + j] = q[blo + j];
+        uint32_t runa = 0, runb = 0;
+        for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            const unsigned long long e = c < C ? fi[c] : 0ull;
+            const uint32_t ca = c < C ? word_a(e) : 0u, cb = c < C ? word_b(e) : 0u;
+            const uint32_t ia = warp_incl_scan(ca), ib = warp_incl_scan(cb);
+            if (c < C) {
+                const uint32_t alo = ps.piece_lo[ps.cta_piece[2 * c]], blo = ps.piece_lo[ps.cta_piece[2 * c + 1]];
+                uint32_t* oa = out + base + runa + ia - ca;
+                uint32_t* ob = out + base + ta + runb + ib - cb;
+                for (uint32_t j = 0; j < ca; ++j) oa[j] = q[alo + j];
+                for (uint32_t j = 0; j < cb; ++j) ob[j] = q[blo + j];
+            }
+            runa += __shfl_sync(0xffffffffu, ia, 31);
+            runb += __shfl_sync(0xffffffffu, ib, 31);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) s_base = base + s_a[C] + s_b[C];
     }
 }
 
-// unpack a remote shard's frames into the ring as publisher `entry`; its
-// pieces start at ids alo / blo
+// unpack a remote shard's frames (b steps from t0) into the ring as publisher
+// `entry`; its pieces start at ids alo / blo.  One block per step.
 template <class M>
-__global__ void k_import(persist_state<M> ps, int64_t t0, const uint32_t* in, uint32_t entry, uint32_t alo,
-                         uint32_t blo) {
-    const uint32_t b = in[0];
-    uint32_t base = 1 + 2 * b;
-    for (uint32_t k = 0; k < b; ++k) {
-        const uint32_t ca = in[1 + 2 * k], cb = in[2 + 2 * k];
-        const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
-        uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
-        for (uint32_t j = threadIdx.x; j < ca; j += blockDim.x) q[alo + j] = in[base + j];
-        for (uint32_t j = threadIdx.x; j < cb; j += blockDim.x) q[blo + j] = in[base + ca + j];
-        if (threadIdx.x == 0)
-            ps.finfo[static_cast<uint64_t>(slot) * ps.E + entry] = frame_word(t0 + k, ca, cb);
-        base += ca + cb;
+__global__ void k_import(persist_state<M> ps, int64_t t0, uint32_t b, const uint32_t* in, uint32_t entry,
+                         uint32_t alo, uint32_t blo) {
+    __shared__ uint32_t s_base;
+    const uint32_t k = blockIdx.x;
+    if (k >= b) return;
+    if (threadIdx.x < 32) {
+        uint32_t before = 0;
+        for (uint32_t q = threadIdx.x; q < k; q += 32) before += in[1 + 2 * q] + in[2 + 2 * q];
+        for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+        if (threadIdx.x == 0) {
+            s_base = 1 + 2 * b + before;
+            if (in[0] != b) ps.flags[2] = 1;  // batch length mismatch between shards
+        }
+    }
+    __syncthreads();
+    const uint32_t ca = in[1 + 2 * k], cb = in[2 + 2 * k], base = s_base;
+    const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
+    uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
+    for (uint32_t j = threadIdx.x; j < ca; j += blockDim.x) q[alo + j] = in[base + j];
+    for (uint32_t j = threadIdx.x; j < cb; j += blockDim.x) q[blo + j] = in[base + ca + j];
+    __syncthreads();
+    if (threadIdx.x == 0) ps.finfo[static_cast<uint64_t>(slot) * ps.E + entry] = frame_word(t0 + k, ca, cb);
+}
+
+// ---- in-engine exchange (NCCL allgather of fixed-size spike bitmasks) ----
+// Rank r's send block: words[0] = b, then for step k < b: wa_max + wb_max
+// words: bit i of the A part = id a_lo_r + i spiked, bit i of the B part =
+// id b_lo_r + i spiked (wa_max / wb_max = the largest A / B range of any
+// rank, in words).  Fixed size, so the allgather needs no counts exchange
+// and no host synchronisation.
+struct xbits_layout {
+    uint32_t wa, wb;   // words per step of the A / B part (max over ranks)
+    uint32_t steps;    // steps per block (delay - 1)
+    uint32_t block;    // words per rank block = 1 + steps * (wa + wb)
+};
+
+// one block per step: this shard's frames -> bitmask (built in shared memory)
+template <class M>
+__global__ void k_export_bits(persist_state<M> ps, int64_t t0, uint32_t b, xbits_layout L, uint32_t a_lo,
+                              uint32_t b_lo, uint32_t* out) {
+    extern __shared__ uint32_t s_bits[];  // wa + wb words
+    const uint32_t k = blockIdx.x;
+    if (k == 0 && threadIdx.x == 0) out[0] = b;
+    if (k >= b) return;
+    const uint32_t W = L.wa + L.wb;
+    for (uint32_t j = threadIdx.x; j < W; j += blockDim.x) s_bits[j] = 0;
+    __syncthreads();
+    const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
+    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(slot) * ps.E;
+    const uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (uint32_t c = warp; c < ps.C; c += nw) {  // warp per local CTA
+        const unsigned long long e = fi[c];
+        const uint32_t ca = word_a(e), cb = word_b(e);
+        const uint32_t alo = ps.piece_lo[ps.cta_piece[2 * c]], blo = ps.piece_lo[ps.cta_piece[2 * c + 1]];
+        for (uint32_t j = lane; j < ca; j += 32) {
+            const uint32_t i = q[alo + j] - a_lo;
+            atomicOr(&s_bits[i >> 5], 1u << (i & 31));
+        }
+        for (uint32_t j = lane; j < cb; j += 32) {
+            const uint32_t i = q[blo + j] - b_lo;
+            atomicOr(&s_bits[L.wa + (i >> 5)], 1u << (i & 31));
+        }
+    }
+    __syncthreads();
+    uint32_t* o = out + 1 + static_cast<uint64_t>(k) * W;
+    for (uint32_t j = threadIdx.x; j < W; j += blockDim.x) o[j] = s_bits[j];
+}
+
+// block (k, rank slot): a remote rank's bitmask of step k -> ascending ids in
+// its pieces' slices of queue slot (t0 + k) % Q, then its frame word
+struct xbits_remote {
+    uint32_t rank, entry, a_lo, b_lo, na, nb;  // rank id, publisher entry, id ranges
+};
+template <class M>
+__global__ void k_import_bits(persist_state<M> ps, int64_t t0, uint32_t b, xbits_layout L, const uint32_t* in,
+                              const xbits_remote* remotes) {
+    __shared__ uint32_t s_scan[33];
+    __shared__ uint32_t s_cnt[2];
+    const uint32_t k = blockIdx.x, rr = blockIdx.y;
+    const xbits_remote R = remotes[rr];
+    const uint32_t* blk = in + static_cast<uint64_t>(R.rank) * L.block;
+    if (k >= b) return;
+    if (k == 0 && threadIdx.x == 0 && blk[0] != b) ps.flags[2] = 1;
+    const uint32_t W = L.wa + L.wb;
+    const uint32_t* bits = blk + 1 + static_cast<uint64_t>(k) * W;
+    const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
+    uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // two parts: A (ids a_lo + i, i < na) then B (ids b_lo + i, i < nb)
+    for (int part = 0; part < 2; ++part) {
+        const uint32_t nwords = part == 0 ? (R.na + 31) / 32 : (R.nb + 31) / 32;
+        const uint32_t* wbits = bits + (part == 0 ? 0u : L.wa);
+        const uint32_t lo = part == 0 ? R.a_lo : R.b_lo;
+        // contiguous chunk of words per thread, block-wide exclusive scan of popcounts
+        const uint32_t per = (nwords + blockDim.x - 1) / blockDim.x;
+        const uint32_t w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
+        uint32_t mine = 0;
+        for (uint32_t w = w0; w < w1; ++w) mine += __popc(wbits[w]);
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        if (lane == 31) s_scan[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t x = lane < nw ? s_scan[lane] : 0u;
+            uint32_t wi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= static_cast<uint32_t>(o)) wi += y;
+            }
+            if (lane < nw) s_scan[lane] = wi - x;
+            if (lane == 31) s_cnt[part] = wi;
+        }
+        __syncthreads();
+        uint32_t pos = s_scan[warp] + incl - mine;
+        for (uint32_t w = w0; w < w1; ++w) {
+            uint32_t m = wbits[w];
+            while (m) {
+                const uint32_t bit = __ffs(m) - 1;
+                m &= m - 1;
+                q[lo + pos++] = lo + w * 32 + bit;
+            }
+        }
+        __syncthreads();  // s_scan reused by the next part
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        ps.finfo[static_cast<uint64_t>(slot) * ps.E + R.entry] = frame_word(t0 + k, s_cnt[0], s_cnt[1]);
     }
 }
 

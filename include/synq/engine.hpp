@@ -48,6 +48,7 @@
 #include "synq/detail/kernels.cuh"
 #include "synq/detail/persistent.cuh"
 #include "synq/detail/pipeline.cuh"
+#include "synq/detail/exchange.hpp"
 #include "synq/models/benchmarks.hpp"
 #include "synq/network_desc.hpp"
 #include "synq/random.hpp"
@@ -73,6 +74,10 @@ struct engine_options {
     // shard_rank of shard_world; frames are exchanged with export/import
     uint32_t shard_rank = 0;
     uint32_t shard_world = 1;
+    // in-engine exchange: every shard passes the same NCCL unique id and the
+    // engine allgathers the spike frames itself after every batch
+    bool shard_nccl = false;
+    std::array<char, 128> nccl_id{};
 };
 
 struct engine_counters {
@@ -185,6 +190,10 @@ public:
         for (auto& sl : slots_)
             for (auto& e : sl.ev)
                 if (e) cudaEventDestroy(e);
+        if (nccl_) {
+            if (stream_) cudaStreamSynchronize(stream_);
+            detail::nccl_comm_destroy(nccl_);
+        }
         if (stream_) {
             cudaStreamSynchronize(stream_);
             cudaStreamDestroy(stream_);
@@ -247,7 +256,7 @@ public:
 
     void run(int64_t steps) {
         if (steps <= 0) return;
-        if (sharded()) {
+        if (sharded() && !nccl_) {
             // a shard may only run steps whose due frames are all present:
             // at most delay-1 steps past the frames imported from every rank
             if (steps > int64_t(delay_) - 1)
@@ -268,9 +277,23 @@ public:
             // into pinned host slots), so the GPU never idles on the host
             int slot = 0;
             bool pending = false;
+            // in-engine exchange: batches of at most delay-1 steps, each
+            // followed by export -> ncclAllGather -> import on this stream
+            const int64_t cap = nccl_ ? std::min<int64_t>(batch_cap_, int64_t(delay_) - 1) : int64_t(batch_cap_);
             while (steps > 0) {
-                const int64_t b = std::min<int64_t>(steps, batch_cap_);
+                const int64_t b = std::min<int64_t>(steps, cap);
+                if constexpr (population_model)
+                    if (nccl_) {
+                        last_batch_t0_ = t_;
+                        last_batch_b_ = static_cast<uint32_t>(b);
+                    }
                 launch_persistent(static_cast<uint32_t>(b), slot);
+                if constexpr (population_model)
+                    if (nccl_) {
+                        enqueue_export_bits(last_batch_t0_, last_batch_b_, xsend_.get());
+                        detail::nccl_allgather_u32(nccl_, xsend_.get(), xrecv_.get(), xl_.block, stream_);
+                        enqueue_import_bits(last_batch_t0_, last_batch_b_, xrecv_.get());
+                    }
                 if (pending) finish_persistent(slot ^ 1);
                 pending = true;
                 slot ^= 1;
@@ -279,7 +302,8 @@ public:
             if (pending) finish_persistent(slot ^ 1);
             pull_counters();
             if (flags_host_[1]) throw device_error("ordered delivery scratch overflow");
-            if (log_on_ && logged_upto_ < t_ && !sharded()) drain_log();
+            if (flags_host_[2]) throw device_error("sharded run: imported frames of a different batch length");
+            if (log_on_ && logged_upto_ < t_ && (!sharded() || nccl_)) drain_log();
         } else {
             while (steps > 0) {
                 const int64_t b = std::min<int64_t>(steps, batch_cap_);
@@ -354,41 +378,57 @@ public:
         if constexpr (population_model) {
             if (!sharded() || !persistent_) throw std::logic_error("export_frames: not a persistent shard");
             const uint64_t need = export_capacity();
-            if (xbuf_.size() < need) xbuf_.resize(need);
-            dev::k_export<Model><<<1, 1024, 0, stream_>>>(pstate(), last_batch_t0_, last_batch_b_, xbuf_.get());
+            // straight into a device destination that can hold the worst case
+            const bool direct = device_dst && cap_words >= need;
+            if (!direct && xbuf_.size() < need) xbuf_.resize(need);
+            uint32_t* out = direct ? static_cast<uint32_t*>(dst) : xbuf_.get();
+            dev::k_export<Model><<<1, 1024, 0, stream_>>>(pstate(), last_batch_t0_, last_batch_b_, out);
             SYNQ_CUDA(cudaGetLastError());
+            launches_ += 1;
             uint64_t words = 1 + 2ull * last_batch_b_;
-            std::vector<uint32_t> counts(2 * size_t(last_batch_b_));
-            if (!counts.empty())
-                SYNQ_CUDA(cudaMemcpyAsync(counts.data(), xbuf_.get() + 1, counts.size() * 4, cudaMemcpyDeviceToHost, stream_));
+            xcounts_.resize(2 * size_t(last_batch_b_) + 1);
+            if (last_batch_b_)
+                SYNQ_CUDA(cudaMemcpyAsync(xcounts_.data(), out + 1, 8ull * last_batch_b_, cudaMemcpyDeviceToHost, stream_));
             SYNQ_CUDA(cudaStreamSynchronize(stream_));
-            for (uint32_t v : counts) words += v;
+            for (uint32_t k = 0; k < 2 * last_batch_b_; ++k) words += xcounts_[k];
             if (words > cap_words) throw std::invalid_argument("export_frames: destination too small");
-            SYNQ_CUDA(cudaMemcpyAsync(dst, xbuf_.get(), words * 4,
-                                      device_dst ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream_));
-            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            if (!direct) {
+                SYNQ_CUDA(cudaMemcpyAsync(dst, xbuf_.get(), words * 4,
+                                          device_dst ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream_));
+                SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            }
             return words;
         } else {
             throw std::logic_error("export_frames: model has no persistent engine");
         }
     }
     // unpack rank `from`'s exported frames (batch starting at the same step
-    // as this shard's last run)
+    // as this shard's last run; every shard runs the same batches).  Stream-
+    // ordered, no host synchronisation: a device source must stay valid
+    // until the next run() (which synchronises).
     void import_frames(const void* src, uint64_t words, uint32_t from, bool device_src) {
         if constexpr (population_model) {
             if (!sharded() || !persistent_) throw std::logic_error("import_frames: not a persistent shard");
             if (from >= opt_.shard_world || from == opt_.shard_rank) throw std::invalid_argument("import_frames: bad rank");
-            if (xbuf_.size() < words) xbuf_.resize(words);
-            SYNQ_CUDA(cudaMemcpyAsync(xbuf_.get(), src, words * 4,
-                                      device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
-            uint32_t b = 0;
-            SYNQ_CUDA(cudaMemcpyAsync(&b, xbuf_.get(), 4, cudaMemcpyDeviceToHost, stream_));
-            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            const uint32_t b = last_batch_b_;
+            if (words < 1 + 2ull * b) throw std::invalid_argument("import_frames: truncated frame words");
+            const uint32_t* in = static_cast<const uint32_t*>(src);
+            if (!device_src) {
+                const size_t slot = from % 2;  // host sources: staged per rank parity (stream-ordered reuse)
+                if (ibuf_[slot].size() < words) {
+                    SYNQ_CUDA(cudaStreamSynchronize(stream_));
+                    ibuf_[slot].resize(words);
+                }
+                SYNQ_CUDA(cudaMemcpyAsync(ibuf_[slot].get(), src, words * 4, cudaMemcpyHostToDevice, stream_));
+                SYNQ_CUDA(cudaStreamSynchronize(stream_));  // the host buffer may be reused by the caller
+                in = ibuf_[slot].get();
+            }
             const int64_t t0 = imported_upto_[from];
-            dev::k_import<Model><<<1, 1024, 0, stream_>>>(pstate(), t0, xbuf_.get(), remote_[from][0],
-                                                         remote_[from][1], remote_[from][2]);
+            if (b)
+                dev::k_import<Model><<<b, 256, 0, stream_>>>(pstate(), t0, b, in, remote_[from][0], remote_[from][1],
+                                                           remote_[from][2]);
             SYNQ_CUDA(cudaGetLastError());
-            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+            launches_ += 1;
             imported_upto_[from] = t0 + b;
         } else {
             throw std::logic_error("import_frames: model has no persistent engine");
@@ -432,7 +472,8 @@ public:
     }
 
     void set_spike_tap(tap_fn fn) {
-        if (fn && sharded()) throw std::invalid_argument("spike taps are not available on a shard");
+        if (fn && sharded() && !opt_.shard_nccl)
+            throw std::invalid_argument("spike taps need the in-engine exchange on a shard");
         tap_ = std::move(fn);
         if (tap_) {
             ensure_log();
@@ -553,6 +594,8 @@ private:
             throw std::invalid_argument("sharding needs the persistent engine (population-delivery model)");
         if (sharded() && delay_ < 2)
             throw std::invalid_argument("sharding needs a delay of at least 2 steps (frames are exchanged every delay-1 steps)");
+        if constexpr (population_model)
+            if (sharded()) setup_exchange();
         Q_ = persistent_ ? 2 * delay_ : delay_;
         queue_.resize(std::max<size_t>(1, size_t(Q_) * n_));
         qcount_.resize(Q_);
@@ -725,6 +768,8 @@ private:
         build_splits(graph_, alo, split_, stream_);
         finfo_.resize(size_t(2) * delay_ * E);
         shard_lo_ = {ra[R], ra[R + 1], ub[R], ub[R + 1]};
+        all_ra_ = ra;
+        all_ub_ = ub;
         imported_upto_.assign(W, 0);
         K_ = K;
         std::copy(bound, bound + dev::kMaxClasses, bound_);
@@ -734,6 +779,75 @@ private:
         persistent_ = true;
     }
 
+    // fixed-size bitmask exchange (detail/persistent.cuh k_export_bits /
+    // k_import_bits); the NCCL communicator only with opt.shard_nccl
+    void setup_exchange() requires population_model {
+        const uint32_t W = opt_.shard_world, R = opt_.shard_rank;
+        uint32_t wa = 1, wb = 1;
+        for (uint32_t q = 0; q < W; ++q) {
+            wa = std::max(wa, (all_ra_[q + 1] - all_ra_[q] + 31) / 32);
+            wb = std::max(wb, (all_ub_[q + 1] - all_ub_[q] + 31) / 32);
+        }
+        xl_ = dev::xbits_layout{wa, wb, delay_ - 1, 1 + (delay_ - 1) * (wa + wb)};
+        if ((wa + wb) * 4ull > 160 * 1024) throw std::invalid_argument("shard exchange: rank range too large");
+        if ((wa + wb) * 4ull > 48 * 1024)
+            SYNQ_CUDA(cudaFuncSetAttribute(dev::k_export_bits<Model>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>((wa + wb) * 4)));
+        std::vector<dev::xbits_remote> rem;
+        for (uint32_t q = 0; q < W; ++q)
+            if (q != R)
+                rem.push_back({q, remote_[q][0], all_ra_[q], all_ub_[q], all_ra_[q + 1] - all_ra_[q],
+                               all_ub_[q + 1] - all_ub_[q]});
+        xremotes_.resize(std::max<size_t>(1, rem.size()) * sizeof(dev::xbits_remote) / 4);
+        if (!rem.empty()) SYNQ_CUDA(cudaMemcpy(xremotes_.get(), rem.data(), rem.size() * sizeof(rem[0]), cudaMemcpyHostToDevice));
+        if (opt_.shard_nccl) {
+            xsend_.resize(xl_.block);
+            xrecv_.resize(size_t(W) * xl_.block);
+            nccl_ = detail::nccl_comm_init(R, W, opt_.nccl_id.data());
+        }
+    }
+
+    // this shard's frames of steps [t0, t0+b) -> its bitmask block at `out`
+    void enqueue_export_bits(int64_t t0, uint32_t b, uint32_t* out) requires population_model {
+        dev::k_export_bits<Model><<<std::max<uint32_t>(1, b), 256, (xl_.wa + xl_.wb) * 4, stream_>>>(
+            pstate(), t0, b, xl_, shard_lo_[0], shard_lo_[2], out);
+        SYNQ_CUDA(cudaGetLastError());
+        launches_ += 1;
+    }
+    // every other rank's block of the gathered buffer -> the ring
+    void enqueue_import_bits(int64_t t0, uint32_t b, const uint32_t* all) requires population_model {
+        const uint32_t W = opt_.shard_world, R = opt_.shard_rank;
+        if (W > 1 && b)
+            dev::k_import_bits<Model><<<dim3(b, W - 1), 256, 0, stream_>>>(
+                pstate(), t0, b, xl_, all, reinterpret_cast<const dev::xbits_remote*>(xremotes_.get()));
+        SYNQ_CUDA(cudaGetLastError());
+        launches_ += 1;
+        for (uint32_t q = 0; q < W; ++q)
+            if (q != R) imported_upto_[q] = t0 + b;
+    }
+
+public:
+    // words per rank block of the bitmask exchange (0 when not sharded)
+    uint64_t exchange_block_words() const { return sharded() ? xl_.block : 0; }
+    // manual bitmask exchange (the in-engine NCCL path does the same after
+    // every batch): export the last run's frames into dst (device, block
+    // words), import every other rank's block of a gathered buffer
+    void export_bits(uint32_t* dst) {
+        if constexpr (population_model) {
+            if (!sharded()) throw std::logic_error("export_bits: not a shard");
+            enqueue_export_bits(last_batch_t0_, last_batch_b_, dst);
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        }
+    }
+    void import_bits(const uint32_t* all) {
+        if constexpr (population_model) {
+            if (!sharded()) throw std::logic_error("import_bits: not a shard");
+            enqueue_import_bits(last_batch_t0_, last_batch_b_, all);
+            SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        }
+    }
+
+private:
     void reset_graph() {
         if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
         graph_exec_ = nullptr;
@@ -1324,9 +1438,15 @@ private:
     dev_array<uint32_t> piece_src_;
     // shard exchange
     std::vector<std::array<uint32_t, 3>> remote_;  // per rank: publisher entry, A lo, B lo
+    std::vector<uint32_t> all_ra_, all_ub_;          // every rank's receiving / update-only ranges
+    dev::xbits_layout xl_{};
+    dev_array<uint32_t> xremotes_, xsend_, xrecv_;
+    void* nccl_ = nullptr;  // ncclComm_t of the in-engine exchange
     std::array<uint32_t, 4> shard_lo_{};           // this shard: A [lo, hi), B [lo, hi)
     std::vector<int64_t> imported_upto_;            // frames < this imported, per rank
-    dev_array<uint32_t> xbuf_;                      // export / import staging
+    dev_array<uint32_t> xbuf_;
+    dev_array<uint32_t> ibuf_[2];
+    std::vector<uint32_t> xcounts_;                      // export / import staging
     int64_t last_batch_t0_ = 0;
     uint32_t last_batch_b_ = 0;
     int npt_select_ = 1;

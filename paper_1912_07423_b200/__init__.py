@@ -137,6 +137,11 @@ def lib() -> C.CDLL:
     sig("synq_sim_shard_export", st, vp, vp, u64, C.c_int, C.POINTER(u64))
     sig("synq_sim_shard_import", st, vp, vp, u64, u32, C.c_int)
     sig("synq_sim_phase_cycles", st, vp, vp, C.POINTER(u32))
+    sig("synq_nccl_unique_id", st, vp)
+    sig("synq_opts_shard_nccl", st, vp, u32, u32, vp)
+    sig("synq_sim_shard_bits_words", u64, vp)
+    sig("synq_sim_shard_export_bits", st, vp, vp)
+    sig("synq_sim_shard_import_bits", st, vp, vp)
     _lib = L
     return L
 
@@ -155,7 +160,8 @@ class Opts:
 
     def __init__(self, seed=None, threads=None, deterministic=None, dt=None, delay=None,
                  record=None, defaults_file=None, params=None, batch_steps=None,
-                 persistent=None, tiles=None, profile=None, shard=None, pipeline=None, lead=0):
+                 persistent=None, tiles=None, profile=None, shard=None, pipeline=None, lead=0,
+                 shard_nccl=None):
         self.h = lib().synq_opts_new()
         if not self.h:
             raise MemoryError("synq_opts_new")
@@ -188,6 +194,10 @@ class Opts:
             check(L.synq_opts_profile(self.h, int(profile)))
         if shard is not None:
             check(L.synq_opts_shard(self.h, int(shard[0]), int(shard[1])))
+        if shard_nccl is not None:  # (rank, world, 128-byte NCCL unique id)
+            rank, world, uid = shard_nccl
+            buf = C.create_string_buffer(bytes(uid), 128)
+            check(L.synq_opts_shard_nccl(self.h, int(rank), int(world), buf))
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -407,6 +417,16 @@ class Sim:
     def set_record(self, on: bool):
         check(lib().synq_sim_set_record(self.h, int(on)))
 
+    # ---- bitmask frame exchange (the in-engine NCCL path does this itself)
+    def shard_bits_words(self) -> int:
+        return int(lib().synq_sim_shard_bits_words(self.h))
+
+    def shard_export_bits(self, device_ptr: int):
+        check(lib().synq_sim_shard_export_bits(self.h, C.c_void_p(device_ptr)))
+
+    def shard_import_bits(self, device_ptr: int):
+        check(lib().synq_sim_shard_import_bits(self.h, C.c_void_p(device_ptr)))
+
     def kernel_launches(self) -> int:
         return int(lib().synq_sim_kernel_launches(self.h))
 
@@ -414,6 +434,14 @@ class Sim:
         out = np.zeros(2, np.uint64)
         check(lib().synq_sim_transfer_bytes(self.h, _p(out)))
         return int(out[0]), int(out[1])
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id for synq_opts_shard_nccl (make it on one
+    rank and broadcast it)."""
+    buf = C.create_string_buffer(128)
+    check(lib().synq_nccl_unique_id(buf))
+    return buf.raw
 
 
 def memory_estimate(model: str, neurons: int, synapses: int) -> dict:

@@ -78,6 +78,9 @@ public:
     virtual std::array<uint32_t, 4> shard_range() const = 0;
     virtual uint64_t shard_export(void* dst, uint64_t cap, bool device) = 0;
     virtual void shard_import(const void* src, uint64_t words, uint32_t from, bool device) = 0;
+    virtual uint64_t shard_bits_words() const = 0;
+    virtual void shard_export_bits(void* dst) = 0;
+    virtual void shard_import_bits(const void* all) = 0;
 
     void write_stats(std::ostream& out) const;
     void write_stats_to(const std::string& path) const;
@@ -143,6 +146,9 @@ public:
     void shard_import(const void* src, uint64_t words, uint32_t from, bool device) override {
         net_->import_frames(src, words, from, device);
     }
+    uint64_t shard_bits_words() const override { return net_->exchange_block_words(); }
+    void shard_export_bits(void* dst) override { net_->export_bits(static_cast<uint32_t*>(dst)); }
+    void shard_import_bits(const void* all) override { net_->import_bits(static_cast<const uint32_t*>(all)); }
     void set_record(bool on) override {
         record_ = on;
         raster_.records.clear();  // keeps its capacity: a recurring recording reuses the pages
@@ -694,6 +700,43 @@ synq_status synq_sim_shard_import(synq_sim* s, const void* src, uint64_t words, 
     SYNQ_CHECK_HANDLE(src);
     return guarded([&] {
         s->impl->shard_import(src, words, from_rank, device != 0);
+        return SYNQ_OK;
+    });
+}
+synq_status synq_nccl_unique_id(void* out) {
+    SYNQ_CHECK_HANDLE(out);
+    return guarded([&] {
+        detail::nccl_unique_id(static_cast<char*>(out));
+        return SYNQ_OK;
+    });
+}
+synq_status synq_opts_shard_nccl(synq_opts* o, uint32_t rank, uint32_t world, const void* id) {
+    SYNQ_CHECK_HANDLE(o);
+    SYNQ_CHECK_HANDLE(id);
+    if (world < 1 || rank >= world) {
+        set_error("shard: need rank < world, world >= 1");
+        return SYNQ_ERR_INVALID_ARGUMENT;
+    }
+    o->cfg.engine.shard_rank = rank;
+    o->cfg.engine.shard_world = world;
+    o->cfg.engine.shard_nccl = true;
+    std::memcpy(o->cfg.engine.nccl_id.data(), id, o->cfg.engine.nccl_id.size());
+    return SYNQ_OK;
+}
+uint64_t synq_sim_shard_bits_words(const synq_sim* s) { return s ? s->impl->shard_bits_words() : 0; }
+synq_status synq_sim_shard_export_bits(synq_sim* s, void* dst) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(dst);
+    return guarded([&] {
+        s->impl->shard_export_bits(dst);
+        return SYNQ_OK;
+    });
+}
+synq_status synq_sim_shard_import_bits(synq_sim* s, const void* all) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(all);
+    return guarded([&] {
+        s->impl->shard_import_bits(all);
         return SYNQ_OK;
     });
 }

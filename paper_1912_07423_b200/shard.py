@@ -144,12 +144,29 @@ class ShardGroup:
     one-GPU stand-in for a multi-GPU run.
     """
 
-    def __init__(self, model: str, neurons: int, world: int, record: bool = False, **opts):
+    def __init__(self, model: str, neurons: int, world: int, record: bool = False, exchange: str = "words",
+                 **opts):
         self.world = world
         self.sims = [Sim(model, neurons, Opts(shard=(r, world), **opts)) for r in range(world)]
         self.delay = self.sims[0].delay
         self.record = record
+        self.exchange = exchange  # "words" (host wire format) or "bits" (the in-engine bitmask blocks)
         self.frames: list[np.ndarray] = []
+        self._gathered = None
+
+    def _bits_exchange(self):
+        """What ncclAllGather does for the in-engine exchange: every rank's
+        bitmask block side by side in one device buffer, imported by all."""
+        import torch
+
+        words = self.sims[0].shard_bits_words()
+        if self._gathered is None:
+            self._gathered = torch.zeros(self.world * words, dtype=torch.int32, device="cuda")
+        g = self._gathered
+        for r, s in enumerate(self.sims):
+            s.shard_export_bits(g.data_ptr() + 4 * r * words)
+        for s in self.sims:
+            s.shard_import_bits(g.data_ptr())
 
     def run(self, steps: int):
         batch = self.delay - 1
@@ -157,11 +174,15 @@ class ShardGroup:
             b = min(steps, batch)
             for s in self.sims:
                 s.run(b)
-            words = [s.shard_export() for s in self.sims]
-            for r, s in enumerate(self.sims):
-                for q in range(self.world):
-                    if q != r:
-                        s.shard_import(words[q], q)
+            if self.exchange == "bits":
+                words = [s.shard_export() for s in self.sims] if self.record else None
+                self._bits_exchange()
+            else:
+                words = [s.shard_export() for s in self.sims]
+                for r, s in enumerate(self.sims):
+                    for q in range(self.world):
+                        if q != r:
+                            s.shard_import(words[q], q)
             if self.record:
                 self.frames.extend(merge_frames(words))
             steps -= b

@@ -25,17 +25,21 @@ def population_runs(golden):
             yield tag, m
 
 
-def group(m, world, **kw):
-    return shard.ShardGroup(m["model"], m["neurons"], world, record=True, seed=m["seed"],
+def group(m, world, exchange="words", **kw):
+    return shard.ShardGroup(m["model"], m["neurons"], world, record=True, seed=m["seed"], exchange=exchange,
                             deterministic=True, dt=m["dt"] or None, delay=m["delay"] or None, **kw)
 
 
+@pytest.mark.parametrize("exchange", ["words", "bits"])
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_sharded_bit_exact(golden, world):
+def test_sharded_bit_exact(golden, world, exchange):
+    """exchange="bits": the fixed-size bitmask blocks of the in-engine NCCL
+    exchange (k_export_bits -> allgather -> k_import_bits), gathered by hand
+    into one device buffer on this GPU."""
     runs = golden["runs"]
     n_cases = 0
     for tag, m in population_runs(golden):
-        g = group(m, world)
+        g = group(m, world, exchange)
         assert all(s.persistent for s in g.sims)
         g.run(m["steps"])
         counts = np.array([len(f) for f in g.frames])
