@@ -117,20 +117,39 @@ SYNQ_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memor
 
 // 32x32 bit transpose across a warp: lane i holds row i on entry, lane b
 // holds column b on exit (bit i = bit b of lane i's entry word).  Stages 16
-// and 8 are byte permutes, stages 4 / 2 / 1 a rotate plus a masked merge.
-SYNQ_DEV uint32_t transpose32(uint32_t x, uint32_t lane) {
-    uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16);
-    x = __byte_perm(x, y, (lane & 16) ? 0x3276u : 0x5410u);
-    y = __shfl_xor_sync(0xffffffffu, x, 8);
-    x = __byte_perm(x, y, (lane & 8) ? 0x3715u : 0x6240u);
+// and 8 are byte permutes, stages 4 / 2 / 1 a rotate plus one LOP3 merge.
+// The per-lane selectors / rotations / merge masks are hoisted (tp_consts).
+struct tp_consts {
+    uint32_t sel16, sel8, rot[3], keep[3];
+};
+SYNQ_DEV tp_consts make_tp_consts(uint32_t lane) {
+    tp_consts k;
+    k.sel16 = (lane & 16) ? 0x3276u : 0x5410u;
+    k.sel8 = (lane & 8) ? 0x3715u : 0x6240u;
 #pragma unroll
-    for (int j = 4; j >= 1; j >>= 1) {
-        const uint32_t m = j == 4 ? 0x0f0f0f0fu : (j == 2 ? 0x33333333u : 0x55555555u);
+    for (int s = 0; s < 3; ++s) {
+        const uint32_t j = 4u >> s;
+        const uint32_t m = s == 0 ? 0x0f0f0f0fu : (s == 1 ? 0x33333333u : 0x55555555u);
         const bool hi = (lane & j) != 0;
-        y = __shfl_xor_sync(0xffffffffu, x, j);
-        const uint32_t t = __funnelshift_l(y, y, hi ? 32 - j : j);
-        const uint32_t keep = hi ? ~m : m;
-        x = (x & keep) | (t & ~keep);
+        k.rot[s] = hi ? 32 - j : j;
+        k.keep[s] = hi ? ~m : m;
+    }
+    return k;
+}
+SYNQ_DEV uint32_t lop3_merge(uint32_t x, uint32_t t, uint32_t keep) {  // (x & keep) | (t & ~keep)
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(x), "r"(t), "r"(keep));
+    return d;
+}
+SYNQ_DEV uint32_t transpose32(uint32_t x, const tp_consts& k) {
+    uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16);
+    x = __byte_perm(x, y, k.sel16);
+    y = __shfl_xor_sync(0xffffffffu, x, 8);
+    x = __byte_perm(x, y, k.sel8);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+        y = __shfl_xor_sync(0xffffffffu, x, 4 >> s);
+        x = lop3_merge(x, __funnelshift_l(y, y, k.rot[s]), k.keep[s]);
     }
     return x;
 }
@@ -158,6 +177,7 @@ __global__ void __launch_bounds__(NT, 1)
     __shared__ uint32_t s_seg[kPipeMaxBatch][kMaxPieces + 1];
     __shared__ unsigned long long s_fval[kPipeMaxBatch][kMaxTiles];
     __shared__ uint32_t s_ok[kPipeMaxBatch];
+    __shared__ uint32_t s_gbeg[32], s_gend[32];  // bitmap delivery: spike range of group frame * 4 + class
     __shared__ uint32_t s_qbase[kPipeMaxBatch];  // queue slot base of frame w of the pass
     __shared__ uint32_t s_cbase[kPipeMaxBatch];  // count-ring slot base of frame w of the pass
     __shared__ uint32_t s_dtmp[DW + 1];
@@ -171,6 +191,10 @@ __global__ void __launch_bounds__(NT, 1)
     for (uint32_t j = tid; j <= P; j += NT) s_lo[j] = ps.piece_lo[j];
     for (uint32_t j = tid; j < P; j += NT) s_psrc[j] = ps.piece_src[j];
     for (uint32_t j = tid; j < ring_words; j += NT) ring[j] = 0;
+    if (tid < 32) {
+        s_gbeg[tid] = 0;
+        s_gend[tid] = 0;
+    }
     if (tid < P_SLOTS) s_prof[tid] = 0;
     if (tid == 0) {
         s_delivered = 0;
@@ -452,6 +476,7 @@ __global__ void __launch_bounds__(NT, 1)
                 // class, target) with warp bit-transposes + popc: one counting
                 // atomic per 32 targets x 32 spikes instead of one per delivery.
                 const uint32_t WQ = ps.wq, wq_sh = WQ == 1 ? 0u : (WQ == 2 ? 1u : (WQ == 4 ? 2u : 3u));
+                const tp_consts tpk = make_tp_consts(lane);
                 uint4* sw = reinterpret_cast<uint4*>(chunks);  // cap x WQ, 16-byte slots swizzled
                 uint32_t* s_src = reinterpret_cast<uint32_t*>(sw + cap * WQ);
                 uint8_t* s_grp = reinterpret_cast<uint8_t*>(s_src + cap);
@@ -460,23 +485,25 @@ __global__ void __launch_bounds__(NT, 1)
                 const uint4* bmw = ps.bm + static_cast<uint64_t>(c) * WQ;
                 for (uint32_t g0 = 0; g0 < S; g0 += cap) {
                     const uint32_t n = min(cap, S - g0);
-                    // (1) spike ids: every thread issues all its 4-byte
-                    // global->shared copies (cp.async, no registers held), then
-                    // one wait: a single latency round per pass
-                    for (uint32_t i = dtid; i < n; i += DT) {
-                        const uint32_t g = g0 + i;
-                        uint32_t w = 0, fw = 0;
+                    // (1) spike ids: one item per (frame, piece); a piece's ids
+                    // are contiguous in the queue slice and in the pass, so no
+                    // search is needed.  Every thread issues all its 4-byte
+                    // global->shared copies (cp.async), then one wait.
 #pragma unroll
-                        for (int q = 1; q < kPipeMaxBatch; ++q)
-                            if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
-                                w = q;
-                                fw = fpre[q];
-                            }
-                        const uint32_t gl = g - fw;
+                    for (int w = 0; w < kPipeMaxBatch; ++w) {
+                        if (static_cast<uint32_t>(w) >= B) break;
                         const uint32_t* seg = s_seg[w];
-                        const uint32_t a = piece_of(seg, P, gl);
-                        cp_async4(s_src + i, ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
-                        s_grp[i] = static_cast<uint8_t>(w);
+                        const uint32_t qb = s_qbase[w], fb0 = fpre[w];
+                        if (fb0 + seg[P] <= g0 || fb0 >= g0 + n) continue;  // frame outside this chunk
+                        for (uint32_t a = dtid; a < P; a += DT) {
+                            const uint32_t o0 = seg[a], o1 = seg[a + 1];
+                            for (uint32_t o = o0; o < o1; ++o) {
+                                const uint32_t gg = fb0 + o;
+                                if (gg < g0 || gg >= g0 + n) continue;
+                                cp_async4(s_src + (gg - g0), ps.queue + qb + s_lo[a] + (o - o0));
+                                s_grp[gg - g0] = static_cast<uint8_t>(w);
+                            }
+                        }
                     }
                     cp_async_wait_all();
                     named_bar(BAR_D, DT);
@@ -498,51 +525,77 @@ __global__ void __launch_bounds__(NT, 1)
                     cp_async_wait_all();
                     named_bar(BAR_D, DT);
                     if (profiling) mark(11);
-                    // (3) count: task = (16-byte column q, block of 32 spikes); two
-                    // independent tasks per iteration
-                    const uint32_t nblk = (n + 31) / 32, ntask = WQ * nblk;
-                    for (uint32_t t0 = dwarp; t0 < ntask; t0 += 2 * DW) {
-                        uint4 x[2];
-                        uint32_t grp[2], qq[2];
-                        bool valid[2];
+                    // (3) count.  Unit = (group G = frame * 4 + class, 16-byte
+                    // column q): the spikes of one group are contiguous in
+                    // the pass, so a unit owns its counters (no atomics),
+                    // accumulates popcounts of the transposed 32-spike blocks
+                    // in registers and adds them to the ring once.
+                    for (uint32_t i = dtid; i < n; i += DT) {  // group boundaries
+                        const uint32_t G = s_grp[i];
+                        if (i == 0 || s_grp[i - 1] != G) s_gbeg[G] = i;
+                        if (i + 1 == n || s_grp[i + 1] != G) s_gend[G] = i + 1;
+                    }
+                    named_bar(BAR_D, DT);
+                    for (uint32_t u = dwarp; u < 32 * WQ; u += DW) {
+                        const uint32_t G = u >> wq_sh, q = u & (WQ - 1);
+                        const uint32_t gb = s_gbeg[G], ge = s_gend[G];
+                        if (ge <= gb) continue;
+                        uint32_t cnt[4] = {0, 0, 0, 0};
+                        const uint32_t blk_end = (ge + 31) >> 5;
+                        uint32_t blk = gb >> 5;
+                        // >= 3 blocks: bit-sliced sum of up to 7 blocks per lane
+                        // (3 planes), then one transpose per plane
+                        while (blk + 3 <= blk_end) {
+                            const uint32_t take = min(7u, blk_end - blk);
+                            uint32_t p0[4] = {0, 0, 0, 0}, p1[4] = {0, 0, 0, 0}, p2[4] = {0, 0, 0, 0};
+                            for (uint32_t v = 0; v < take; ++v) {
+                                const uint32_t gs = (blk + v) * 32 + lane;
+                                const bool in = gs >= gb && gs < ge;
+                                const uint4 x = in ? sw[gs * WQ + (q ^ ((gs >> swz_sh) & swz_m))] : make_uint4(0, 0, 0, 0);
+                                const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const uint32_t t = t0 + u * DW;
-                            const uint32_t blk = t >> wq_sh, q = t & (WQ - 1);
-                            const uint32_t g = blk * 32 + lane;
-                            qq[u] = q;
-                            valid[u] = t < ntask && g < n;
-                            x[u] = make_uint4(0, 0, 0, 0);
-                            grp[u] = 0xffu;
-                            if (valid[u]) {
-                                x[u] = sw[g * WQ + (q ^ ((g >> swz_sh) & swz_m))];
-                                grp[u] = s_grp[g];
+                                for (int e = 0; e < 4; ++e) {
+                                    const uint32_t c0 = p0[e] & wv[e];
+                                    p0[e] ^= wv[e];
+                                    const uint32_t c1 = p1[e] & c0;
+                                    p1[e] ^= c0;
+                                    p2[e] ^= c1;  // at most 7 blocks: no carry out of plane 2
+                                }
+                            }
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                cnt[e] += __popc(transpose32(p0[e], tpk)) + (__popc(transpose32(p1[e], tpk)) << 1) +
+                                          (__popc(transpose32(p2[e], tpk)) << 2);
+                            blk += take;
+                        }
+                        for (; blk < blk_end; blk += 2) {
+                            uint4 x[2];
+                            unsigned m[2];
+#pragma unroll
+                            for (int v = 0; v < 2; ++v) {
+                                const uint32_t b0 = (blk + v) * 32, gs = b0 + lane;
+                                const bool in = gs >= gb && gs < ge;
+                                x[v] = in ? sw[gs * WQ + (q ^ ((gs >> swz_sh) & swz_m))] : make_uint4(0, 0, 0, 0);
+                                m[v] = __ballot_sync(0xffffffffu, in);
+                            }
+#pragma unroll
+                            for (int v = 0; v < 2; ++v) {
+                                cnt[0] += __popc(transpose32(x[v].x, tpk) & m[v]);
+                                cnt[1] += __popc(transpose32(x[v].y, tpk) & m[v]);
+                                cnt[2] += __popc(transpose32(x[v].z, tpk) & m[v]);
+                                cnt[3] += __popc(transpose32(x[v].w, tpk) & m[v]);
                             }
                         }
+                        uint32_t* cb = ring + s_cbase[G >> 2] + (G & 3u) * ps.win_cap + q * 128 + lane;
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            x[u].x = transpose32(x[u].x, lane);
-                            x[u].y = transpose32(x[u].y, lane);
-                            x[u].z = transpose32(x[u].z, lane);
-                            x[u].w = transpose32(x[u].w, lane);
-                        }
-#pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            unsigned rem = __ballot_sync(0xffffffffu, valid[u]);
-                            while (rem) {
-                                const uint32_t G = __shfl_sync(0xffffffffu, grp[u], __ffs(rem) - 1);
-                                const unsigned gm = __ballot_sync(0xffffffffu, grp[u] == G);
-                                rem &= ~gm;
-                                uint32_t* cb = ring + s_cbase[G >> 2] + (G & 3u) * ps.win_cap + qq[u] * 128 + lane;
-                                const uint32_t c0 = __popc(x[u].x & gm), c1 = __popc(x[u].y & gm);
-                                const uint32_t c2 = __popc(x[u].z & gm), c3 = __popc(x[u].w & gm);
-                                if (c0) atomicAdd(cb, c0);
-                                if (c1) atomicAdd(cb + 32, c1);
-                                if (c2) atomicAdd(cb + 64, c2);
-                                if (c3) atomicAdd(cb + 96, c3);
-                                my_deliv += c0 + c1 + c2 + c3;
-                            }
-                        }
+                        for (int e = 0; e < 4; ++e)
+                            if (cnt[e]) cb[e * 32] += cnt[e];
+                        my_deliv += cnt[0] + cnt[1] + cnt[2] + cnt[3];
+                    }
+                    named_bar(BAR_D, DT);
+                    for (uint32_t i = dtid; i < 32; i += DT) {  // reset the group table
+                        s_gbeg[i] = 0;
+                        s_gend[i] = 0;
                     }
                     named_bar(BAR_D, DT);  // counts complete, staging reusable
                     if (profiling) mark(P_DELIVER);
