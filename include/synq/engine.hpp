@@ -940,9 +940,24 @@ private:
         if (const char* e = std::getenv("SYNQ_PIPELINE")) mode = std::atoi(e);
         if (mode == 0) return false;
         if (uint64_t(n_) * (graph_.pitch / 4) >= (1ull << 32)) return false;  // 32-bit chunk indices
-        // update warps: 8 once a CTA holds more than 512 neurons (the update's
+        // bitmap delivery when the receive-window bitmaps are clearly smaller
+        // than the ELL rows (dense connectivity, e.g. Brunel p = 0.1)
+        const uint32_t C = static_cast<uint32_t>(alo.size()) - 1;
+        uint32_t wq = (wcap + 127) / 128;
+        wq = wq <= 1 ? 1 : (wq <= 2 ? 2 : (wq <= 4 ? 4 : 8));
+        const uint64_t bm_bytes = uint64_t(n_) * C * wq * 16, ell_bytes = uint64_t(n_) * graph_.pitch * 4;
+        bool use_bm = wcap <= 1024 && 3 * bm_bytes < 2 * ell_bytes && K <= 4;
+        // SYNQ_BITMAP: 0 = never, 1 = when smaller (default), 2 = whenever it fits
+        if (const char* e = std::getenv("SYNQ_BITMAP")) {
+            const int v = std::atoi(e);
+            use_bm = v == 0 ? false : (v == 2 ? (wcap <= 1024 && K <= 4) : use_bm);
+        }
+        pipe_bm_ = use_bm;
+        // update warps: bitmap delivery runs 1024-thread CTAs (16 update + 16
+        // delivery warps) whenever a CTA holds <= 1024 neurons (best at B1e9);
+        // otherwise 8 once a CTA holds more than 512 neurons (the update's
         // per-thread chain is the critical path), else 4 (more deliverers)
-        uint32_t uw_pref = longest > 512 ? 8 : 4;
+        uint32_t uw_pref = (use_bm && longest <= 1024) ? 16 : (longest > 512 ? 8 : 4);
         if (const char* e = std::getenv("SYNQ_UW")) uw_pref = static_cast<uint32_t>(std::atoi(e));
         pipe_threads_ = dev::kPipeThreads;
         if (uw_pref == 16 && longest <= 16 * 32 * 2) {  // 1024-thread CTAs: 16 update + 16 delivery warps
@@ -962,24 +977,13 @@ private:
             return false;
         }
         pipe_ = true;
-        // bitmap delivery when the receive-window bitmaps are clearly smaller
-        // than the ELL rows (dense connectivity, e.g. Brunel p = 0.1)
-        const uint32_t C = static_cast<uint32_t>(alo.size()) - 1;
-        uint32_t wq = (wcap + 127) / 128;
-        wq = wq <= 1 ? 1 : (wq <= 2 ? 2 : (wq <= 4 ? 4 : 8));
-        const uint64_t bm_bytes = uint64_t(n_) * C * wq * 16, ell_bytes = uint64_t(n_) * graph_.pitch * 4;
-        bool use_bm = wcap <= 1024 && 3 * bm_bytes < 2 * ell_bytes && K <= 4;
-        // SYNQ_BITMAP: 0 = never, 1 = when smaller (default), 2 = whenever it fits
-        if (const char* e = std::getenv("SYNQ_BITMAP")) {
-            const int v = std::atoi(e);
-            use_bm = v == 0 ? false : (v == 2 ? (wcap <= 1024 && K <= 4) : use_bm);
-        }
-        pipe_bm_ = use_bm;
         cudaFuncAttributes attr{};
         SYNQ_CUDA(cudaFuncGetAttributes(&attr, kernel_fn()));
         const size_t avail = max_smem > attr.sharedSizeBytes ? max_smem - attr.sharedSizeBytes : 0;
-        // L2 row prefetch pays once the adjacency outgrows L2
-        bool prefetch = graph_.pitch * 4ull * n_ > (64ull << 20);
+        // L2 row prefetch at publish: pays for the ELL delivery once the
+        // adjacency outgrows L2; the bitmap windows are read fast enough
+        // without it (measured: same step time, fewer update instructions)
+        bool prefetch = !use_bm && graph_.pitch * 4ull * n_ > (64ull << 20);
         if (const char* e = std::getenv("SYNQ_PREFETCH")) prefetch = std::atoi(e) != 0;
         const uint32_t pf_cap = prefetch && !use_bm ? ((longest + 1) & ~1u) : 0;
         const size_t slot_bytes = size_t(K) * wcap * 4;

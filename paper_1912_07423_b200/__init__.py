@@ -324,11 +324,16 @@ class Sim:
         check(lib().synq_sim_memory_actual(self.h, C.byref(m)))
         return m.as_dict()
 
-    def raster(self):
+    def raster(self, out=None):
+        """(steps, ids) of the recorded raster.  `out` = (int64, uint32) arrays
+        to fill (grown when too small) lets a caller reuse its buffers."""
         n = C.c_uint64()
         check(lib().synq_sim_raster_size(self.h, C.byref(n)))
-        steps = np.empty(max(n.value, 1), np.int64)
-        ids = np.empty(max(n.value, 1), np.uint32)
+        if out is not None and len(out[0]) >= n.value and len(out[1]) >= n.value:
+            steps, ids = out
+        else:
+            steps = np.empty(max(n.value, 1), np.int64)
+            ids = np.empty(max(n.value, 1), np.uint32)
         check(lib().synq_sim_raster_copy(self.h, _p(steps), _p(ids), n.value))
         return steps[: n.value], ids[: n.value]
 
