@@ -54,7 +54,7 @@
 namespace synq::dev {
 
 constexpr int kPipeThreads = 512;
-constexpr int kPipeMaxBatch = 8;  // frames per delivery pass
+constexpr int kPipeMaxBatch = 8;  // frames per delivery pass (group ids frame * 4 + class < 32)
 
 SYNQ_DEV uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 SYNQ_DEV void st_release_cta(uint32_t* p, uint32_t v) {
@@ -165,7 +165,10 @@ __global__ void __launch_bounds__(NT, 1)
     constexpr int NW = NT / 32;
     constexpr int UT = UW * 32, DT = NT - UT, DW = NW - UW;
     constexpr uint32_t BAR_U = 1, BAR_D = 2;
-    static_assert(DW >= kPipeMaxBatch, "one polling warp per frame of a pass");
+    // frames per delivery pass: one polling warp per frame
+    constexpr int MB = DW < kPipeMaxBatch ? DW : kPipeMaxBatch;
+    static_assert(MB >= 4, "at least 4 delivery warps");
+    static_assert(4 * MB <= 32, "bitmap group tables hold 32 (frame, class) groups");
 
     // dynamic: count ring (R x K x win_cap) | row prefetch windows (pf) | chunk list
     extern __shared__ __align__(16) uint32_t ring[];
@@ -174,12 +177,12 @@ __global__ void __launch_bounds__(NT, 1)
     uint2* chunks = pf + ps.pf_cap;
     __shared__ uint32_t s_lo[kMaxPieces + 1];
     __shared__ uint32_t s_psrc[kMaxPieces];
-    __shared__ uint32_t s_seg[kPipeMaxBatch][kMaxPieces + 1];
-    __shared__ unsigned long long s_fval[kPipeMaxBatch][kMaxTiles];
-    __shared__ uint32_t s_ok[kPipeMaxBatch];
+    __shared__ uint32_t s_seg[MB][kMaxPieces + 1];
+    __shared__ unsigned long long s_fval[MB][kMaxTiles];
+    __shared__ uint32_t s_ok[MB];
     __shared__ uint32_t s_gbeg[32], s_gend[32];  // bitmap delivery: spike range of group frame * 4 + class
-    __shared__ uint32_t s_qbase[kPipeMaxBatch];  // queue slot base of frame w of the pass
-    __shared__ uint32_t s_cbase[kPipeMaxBatch];  // count-ring slot base of frame w of the pass
+    __shared__ uint32_t s_qbase[MB];  // queue slot base of frame w of the pass
+    __shared__ uint32_t s_cbase[MB];  // count-ring slot base of frame w of the pass
     __shared__ uint32_t s_dtmp[DW + 1];
     __shared__ uint32_t s_wa[NPT * UW], s_wb[NPT * UW], s_mw[UW], s_out[3];
     __shared__ uint32_t s_delivered;  // frames delivered: rel 0 .. s_delivered
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(NT, 1)
             // ---- poll: warp w takes frame rel r_next + w (warp 0 waits)
             // (frame f is taken once frame f + lag is complete: the
             // publishers streamed the rows of f into L2 meanwhile)
-            if (dwarp < static_cast<uint32_t>(kPipeMaxBatch)) {
+            if (dwarp < static_cast<uint32_t>(MB)) {
                 const uint32_t r = r_next + dwarp;
                 bool ok = false;
                 if (dwarp == 0) {
@@ -449,10 +452,10 @@ __global__ void __launch_bounds__(NT, 1)
             named_bar(BAR_D, DT);
             if (profiling) mark(10);
             uint32_t B = 0;
-            uint32_t fpre[kPipeMaxBatch + 1];
+            uint32_t fpre[MB + 1];
             fpre[0] = 0;
 #pragma unroll
-            for (int w = 0; w < kPipeMaxBatch; ++w) {
+            for (int w = 0; w < MB; ++w) {
                 const bool take = (static_cast<uint32_t>(w) == B) && s_ok[w];
                 if (take) ++B;
                 fpre[w + 1] = fpre[w] + (take ? s_seg[w][P] : 0u);
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(NT, 1)
             }
             uint32_t flog = 0;
 #pragma unroll
-            for (int q = 1; q <= kPipeMaxBatch; ++q)
+            for (int q = 1; q <= MB; ++q)
                 if (static_cast<uint32_t>(q) == wlog) flog = fpre[q];
             const unsigned long long lbase = lc - flog;
             if constexpr (BM) {
@@ -490,7 +493,7 @@ __global__ void __launch_bounds__(NT, 1)
                     // search is needed.  Every thread issues all its 4-byte
                     // global->shared copies (cp.async), then one wait.
 #pragma unroll
-                    for (int w = 0; w < kPipeMaxBatch; ++w) {
+                    for (int w = 0; w < MB; ++w) {
                         if (static_cast<uint32_t>(w) >= B) break;
                         const uint32_t* seg = s_seg[w];
                         const uint32_t qb = s_qbase[w], fb0 = fpre[w];
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(NT, 1)
                     if (g < S) {
                         uint32_t w = 0, fw = 0;
     #pragma unroll
-                        for (int q = 1; q < kPipeMaxBatch; ++q)
+                        for (int q = 1; q < MB; ++q)
                             if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
                                 w = q;
                                 fw = fpre[q];
