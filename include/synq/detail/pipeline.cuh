@@ -54,6 +54,7 @@
 namespace synq::dev {
 
 constexpr int kPipeThreads = 512;
+constexpr int kStreamChunks = 64;  // streamed update: up to 64 x UT neurons per CTA
 constexpr int kPipeMaxBatch = 8;  // frames per delivery pass (group ids frame * 4 + class < 32)
 
 SYNQ_DEV uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -184,7 +185,10 @@ __global__ void __launch_bounds__(NT, 1)
     __shared__ uint32_t s_qbase[MB];  // queue slot base of frame w of the pass
     __shared__ uint32_t s_cbase[MB];  // count-ring slot base of frame w of the pass
     __shared__ uint32_t s_dtmp[DW + 1];
-    __shared__ uint32_t s_wa[NPT * UW], s_wb[NPT * UW], s_mw[UW], s_out[3];
+    __shared__ uint32_t s_wa[(NPT > 0 ? NPT : 1) * UW], s_wb[(NPT > 0 ? NPT : 1) * UW], s_mw[UW], s_out[3];
+    // streamed update (NPT == 0): per (chunk, warp) spike counts and ballots
+    constexpr int kSE = NPT == 0 ? kStreamChunks * UW : 1;
+    __shared__ uint32_t s_sa[kSE], s_sb[kSE], s_spk[kSE];
     __shared__ uint32_t s_delivered;  // frames delivered: rel 0 .. s_delivered
     __shared__ uint32_t s_updated;    // update steps whose fold is done
     __shared__ unsigned long long s_prof[P_SLOTS];
@@ -229,12 +233,137 @@ __global__ void __launch_bounds__(NT, 1)
         }
     };
 
-    if (warp < static_cast<uint32_t>(UW)) {
+    if (NPT == 0 && warp < static_cast<uint32_t>(UW)) {
+        // ============================================ update warps, streamed
+        // NPT == 0: more neurons per CTA than registers hold (up to
+        // kStreamChunks * UT).  The state stays in HBM (SoA, coalesced) and is
+        // loaded, updated and stored every step in chunks of UT neurons; the
+        // spike flags go through a shared-memory bitmask.
+        const uint32_t lead = min(ps.lead, ps.delay);
+        const uint32_t L = na + nb, MC = (L + UT - 1) / UT;
+        unsigned long long my_spikes = 0;
+        uint32_t slot = static_cast<uint32_t>(t0 % ps.Q);
+        for (uint32_t s = 0; s < nrel; ++s, slot = slot + 1 == ps.Q ? 0u : slot + 1) {
+            const int64_t t = t0 + s;
+            uint32_t* qslot = ps.queue + static_cast<uint64_t>(slot) * ps.n;
+            if (warp == 0) wait_at_least(&s_delivered, min(min(s + ps.delay - lead, s + R - 1), nrel));
+            named_bar(BAR_U, UT);
+            mark(P_POLL);
+            uint32_t* cslot = ring + (s % R) * ps.K * ps.win_cap;
+            uint32_t mcount = 0;
+            for (uint32_t m = 0; m < MC; ++m) {
+                const uint32_t j = tid + m * UT;
+                bool sp = false;
+                if (j < L) {
+                    const uint32_t i = id_of(j);
+                    values_t<NF> vl;
+                    load_all(ps.nf, i, vl);
+                    if (j < na) {  // receiving neuron: fold frame rel s in class order
+                        float acc = detail::pack_get<ACC>::get(vl);
+                        for (int k = 0; k < ps.K; ++k) {
+                            const uint32_t a = cslot[k * ps.win_cap + j];
+                            if (a) {
+                                cslot[k * ps.win_cap + j] = 0;
+                                acc = fold_arrivals(acc, a, ps.delta[k]);
+                            }
+                        }
+                        detail::pack_get<ACC>::get(vl) = acc;
+                    }
+                    xorshift rl;
+                    bool ll = false;
+                    local_neuron<NF> ref{i, &vl, &rl, &ll, ps.rng};
+                    sp = model.update(ref, ps.dt);
+                    store_all(ps.nf, i, vl);
+                    if constexpr (model_uses_rng<M>())
+                        if (ll) ps.rng[i] = rl;
+                    if (sp && i >= ps.meas_lo && i < ps.meas_hi) ++mcount;
+                }
+                const int na_here = static_cast<int>(na) - static_cast<int>(m * UT + warp * 32);
+                const unsigned amask = na_here >= 32 ? 0xffffffffu : (na_here <= 0 ? 0u : (1u << na_here) - 1u);
+                const unsigned bal = __ballot_sync(0xffffffffu, sp);
+                if (lane == 0) {
+                    s_sa[m * UW + warp] = __popc(bal & amask);
+                    s_sb[m * UW + warp] = __popc(bal & ~amask);
+                    s_spk[m * UW + warp] = bal;
+                }
+            }
+            for (int o = 16; o; o >>= 1) mcount += __shfl_xor_sync(0xffffffffu, mcount, o);
+            if (lane == 0) s_mw[warp] = mcount;
+            mark(P_UPDATE);
+            named_bar(BAR_U, UT);  // counts, flags and the slot zeroing are complete
+            if (tid == 0) st_release_cta(&s_updated, s + 1);
+            if (warp == 0) {  // exclusive scans in ascending local index: (chunk, warp) order
+                uint32_t runa = 0, runb = 0;
+                for (uint32_t e0 = 0; e0 < MC * UW; e0 += 32) {
+                    const uint32_t e = e0 + lane;
+                    const uint32_t xa = e < MC * UW ? s_sa[e] : 0u, xb = e < MC * UW ? s_sb[e] : 0u;
+                    const uint32_t ia = warp_incl_scan(xa), ib = warp_incl_scan(xb);
+                    if (e < MC * UW) {
+                        s_sa[e] = runa + ia - xa;
+                        s_sb[e] = runb + ib - xb;
+                    }
+                    runa += __shfl_sync(0xffffffffu, ia, 31);
+                    runb += __shfl_sync(0xffffffffu, ib, 31);
+                }
+                uint32_t mm = lane < UW ? s_mw[lane] : 0;
+                for (int o = 16; o; o >>= 1) mm += __shfl_xor_sync(0xffffffffu, mm, o);
+                if (lane == 0) {
+                    s_out[0] = runa;
+                    s_out[1] = runb;
+                    s_out[2] = mm;
+                }
+            }
+            named_bar(BAR_U, UT);
+            mark(9);
+            const unsigned below = (1u << lane) - 1u;
+            for (uint32_t m = 0; m < MC; ++m) {
+                const uint32_t j = tid + m * UT;
+                const unsigned bal = s_spk[m * UW + warp];
+                if ((bal >> lane) & 1u) {
+                    const int na_here = static_cast<int>(na) - static_cast<int>(m * UT + warp * 32);
+                    const unsigned amask = na_here >= 32 ? 0xffffffffu : (na_here <= 0 ? 0u : (1u << na_here) - 1u);
+                    if (j < na)
+                        qslot[alo + s_sa[m * UW + warp] + __popc(bal & amask & below)] = id_of(j);
+                    else
+                        qslot[blo + s_sb[m * UW + warp] + __popc(bal & ~amask & below)] = id_of(j);
+                }
+            }
+            const uint32_t outa = s_out[0], outb = s_out[1], meas = s_out[2];
+            named_bar(BAR_U, UT);  // piece slices complete (and s_out / s_s* reusable)
+            if (tid == 0) {
+                st_release_gpu(ps.finfo + static_cast<uint64_t>(slot) * ps.E + c, frame_word(t, outa, outb));
+                if (outa + outb) atomicAdd(&ps.step_spikes[s], outa + outb);
+                if (meas) atomicAdd(&ps.step_meas[s], meas);
+                my_spikes += outa + outb;
+            }
+            mark(P_PUBLISH);
+        }
+        named_bar(BAR_U, UT);
+        // fold the last delivered frame (rel nsteps) into ACC
+        wait_at_least(&s_delivered, nrel);
+        const uint32_t* cl = ring + (nrel % R) * ps.K * ps.win_cap;
+        for (uint32_t j = tid; j < na; j += UT) {
+            uint32_t a[kMaxClasses];
+            bool any = false;
+            for (int k = 0; k < ps.K; ++k) {
+                a[k] = cl[k * ps.win_cap + j];
+                any |= a[k] != 0;
+            }
+            if (any) {
+                auto* accp = &ps.nf.template get<ACC>()[alo + j];
+                float acc = *accp;
+                for (int k = 0; k < ps.K; ++k) acc = fold_arrivals(acc, a[k], ps.delta[k]);
+                *accp = acc;
+            }
+        }
+        if (tid == 0 && my_spikes) atomicAdd(&ps.counters[C_SPIKES], my_spikes);
+        if (profiling) s_prof[P_STEPS] = static_cast<unsigned long long>(nsteps);
+    } else if (NPT != 0 && warp < static_cast<uint32_t>(UW)) {
         // ============================================ update warps
         const uint32_t lead = min(ps.lead, ps.delay);
-        values_t<NF> v[NPT];
-        xorshift rr[NPT];
-        bool live[NPT];
+        values_t<NF> v[NPT > 0 ? NPT : 1];
+        xorshift rr[NPT > 0 ? NPT : 1];
+        bool live[NPT > 0 ? NPT : 1];
 #pragma unroll
         for (int r = 0; r < NPT; ++r) {
             live[r] = false;
@@ -255,7 +384,7 @@ __global__ void __launch_bounds__(NT, 1)
             named_bar(BAR_U, UT);
             mark(P_POLL);
             uint32_t* cslot = ring + (s % R) * ps.K * ps.win_cap;
-            bool spk[NPT];
+            bool spk[NPT > 0 ? NPT : 1];
             uint32_t mcount = 0;
 #pragma unroll
             for (int r = 0; r < NPT; ++r) {

@@ -688,7 +688,7 @@ private:
             longest = std::max(longest, (alo[c + 1] - alo[c]) + (blo[c + 1] - blo[c]));
             wcap = std::max(wcap, alo[c + 1] - alo[c]);
         }
-        const bool pipe_fits = longest <= 2048 && uint64_t(n_) * (graph_.pitch / 4) < (1ull << 32);
+        const bool pipe_fits = longest <= uint32_t(dev::kStreamChunks) * 256 && uint64_t(n_) * (graph_.pitch / 4) < (1ull << 32);
         if (longest > max_local && !pipe_fits) return;  // cannot hold the state: per-step kernel graph
         npt_ = longest <= NTH ? 1 : (longest <= 2 * NTH ? 2 : 4);
         // pieces in id order; publishers: local CTAs 0..C-1, then remote shards
@@ -960,7 +960,12 @@ private:
         uint32_t uw_pref = (use_bm && longest <= 1024) ? 16 : (longest > 512 ? 8 : 4);
         if (const char* e = std::getenv("SYNQ_UW")) uw_pref = static_cast<uint32_t>(std::atoi(e));
         pipe_threads_ = dev::kPipeThreads;
-        if (uw_pref == 16 && longest <= 16 * 32 * 2) {  // 1024-thread CTAs: 16 update + 16 delivery warps
+        bool force_stream = false;  // SYNQ_STREAM=1: state in HBM even when registers would hold it (tests)
+        if (const char* e = std::getenv("SYNQ_STREAM")) force_stream = std::atoi(e) != 0;
+        if (force_stream && longest <= uint32_t(dev::kStreamChunks) * 8 * 32) {
+            pipe_uw_ = 8;
+            pipe_npt_ = 0;
+        } else if (uw_pref == 16 && longest <= 16 * 32 * 2) {  // 1024-thread CTAs: 16 update + 16 delivery warps
             pipe_uw_ = 16;
             pipe_npt_ = longest <= 512 ? 1 : 2;
             pipe_threads_ = 1024;
@@ -973,6 +978,9 @@ private:
         } else if (longest <= 8 * 32 * 8) {
             pipe_uw_ = 8;
             pipe_npt_ = 8;
+        } else if (longest <= uint32_t(dev::kStreamChunks) * 8 * 32) {
+            pipe_uw_ = 8;
+            pipe_npt_ = 0;  // streamed: the neuron state stays in HBM
         } else {
             return false;
         }
@@ -983,7 +991,7 @@ private:
         // L2 row prefetch at publish: pays for the ELL delivery once the
         // adjacency outgrows L2; the bitmap windows are read fast enough
         // without it (measured: same step time, fewer update instructions)
-        bool prefetch = !use_bm && graph_.pitch * 4ull * n_ > (64ull << 20);
+        bool prefetch = !use_bm && pipe_npt_ != 0 && graph_.pitch * 4ull * n_ > (64ull << 20);
         if (const char* e = std::getenv("SYNQ_PREFETCH")) prefetch = std::atoi(e) != 0;
         const uint32_t pf_cap = prefetch && !use_bm ? ((longest + 1) & ~1u) : 0;
         const size_t slot_bytes = size_t(K) * wcap * 4;
@@ -1037,6 +1045,7 @@ private:
             return reinterpret_cast<const void*>(dev::k_pipeline<Model, 16, 2, BM, 1024>);
         }
         if (uw == 8) {
+            if (npt == 0) return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 0, BM>);
             if (npt <= 4) return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 4, BM>);
             return reinterpret_cast<const void*>(dev::k_pipeline<Model, 8, 8, BM>);
         }

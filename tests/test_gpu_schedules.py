@@ -25,7 +25,7 @@ pytestmark = pytest.mark.gpu
 
 
 def build(m, env, monkeypatch, **kw):
-    for k in ("SYNQ_BITMAP", "SYNQ_UW", "SYNQ_LAG", "SYNQ_LEAD", "SYNQ_PREFETCH"):
+    for k in ("SYNQ_BITMAP", "SYNQ_UW", "SYNQ_LAG", "SYNQ_LEAD", "SYNQ_PREFETCH", "SYNQ_STREAM"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, str(v))
@@ -115,4 +115,17 @@ def test_batch_boundaries_and_recording(golden, monkeypatch, engine):
     for i in range(3):
         assert np.array_equal(sim.neuron_field(i).view(np.uint32), golden["runs"][f"{tag}_f{i}"])
     assert sim.counters()["deliveries"] == m["counters"]["deliveries"]
+    sim.close()
+
+
+@pytest.mark.parametrize("tag", ["brunel_20000_s1_t2000_h0_d0", "brunel_2000_s99_t3000_h0_d0",
+                                 "vogels_1000_s99_t3000_h0_d0", "vogels_500_s3_t500_h0_d3"])
+@pytest.mark.parametrize("bitmap", [0, 2])
+def test_streamed_state(golden, monkeypatch, tag, bitmap):
+    """Streamed update (neuron state in HBM, loaded / stored every step; the
+    mode for more neurons per CTA than registers hold, e.g. the p <= 0.01
+    sweep networks), forced on the golden networks."""
+    sim = build(golden["meta"]["runs"][tag], {"SYNQ_STREAM": 1, "SYNQ_BITMAP": bitmap}, monkeypatch, pipeline=1)
+    assert sim.pipelined
+    check(sim, golden, tag)
     sim.close()
