@@ -10,8 +10,8 @@
 //                   a single-pass decoupled look-back scan over id tiles; bit
 //                   history + expiry (plastic models).
 //   k_catchup       Update Synapses (lazy STDP, engine.hpp:343-367, 414-436):
-//                   warp per neuron of frame(due) U expiring; each lane
-//                   replays its synapse in registers over [ages, t] against
+//                   CTA per neuron of frame(due) U expiring; each thread
+//                   replays its synapses in registers over [ages, t] against
 //                   the neuron-major bit history, stores once.
 //   k_receive       Receive Spikes (engine.hpp:369-409): warp per
 //                   (spike, 256-target chunk); deliveries through device
@@ -341,11 +341,10 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
     } else {
         total = st.n;
     }
-    const uint32_t lane = lane_id();
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    // one CTA per neuron (grid-stride): its synapses replay blockDim.x at a
+    // time, so the serial replay chains of many synapses overlap
     constexpr uint32_t kMaxWords = 4;
-    for (uint32_t k = warp; k < total; k += nwarps) {
+    for (uint32_t k = blockIdx.x; k < total; k += gridDim.x) {
         const uint32_t nid = mode == 1 ? k : (k < ntr ? frame[k] : st.expiring[k - ntr]);
         const int64_t a0 = st.ages[nid];
         if (a0 > through) continue;
@@ -357,7 +356,7 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
 #pragma unroll
         for (uint32_t w = 0; w < kMaxWords; ++w)
             pre[w] = w < W ? st.hist[static_cast<uint64_t>(nid) * W + w] : 0;
-        for (uint32_t kk = lane; kk < d; kk += 32) {
+        for (uint32_t kk = threadIdx.x; kk < d; kk += blockDim.x) {
             const uint32_t dst = row[kk];
             uint64_t post[kMaxWords];
 #pragma unroll
@@ -368,13 +367,27 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
             const synapse_state<SF> s0 = s;
             s.src_ = nid;
             s.dst_ = dst;
-            for (int64_t u = a0; u <= through; ++u)
-                model.update_synapse(s, word_bit(pre, W, u - static_cast<int64_t>(st.delay)),
-                                     word_bit(post, W, u), st.dt);
+            // replay [a0, through]: ring positions advance incrementally (no
+            // 64-bit modulo per step); words picked from registers
+            const uint32_t HB = 64u * W;
+            int64_t upre = a0 - static_cast<int64_t>(st.delay);
+            uint32_t sp = static_cast<uint32_t>(a0 % HB);
+            uint32_t spre = upre >= 0 ? static_cast<uint32_t>(upre % HB) : 0u;
+            auto pick = [](const uint64_t* w, uint32_t slot) {
+                const uint32_t q = slot >> 6;
+                const uint64_t v = q == 0 ? w[0] : (q == 1 ? w[1] : (q == 2 ? w[2] : w[3]));
+                return ((v >> (slot & 63)) & 1ull) != 0;
+            };
+            for (int64_t u = a0; u <= through; ++u) {
+                const bool pb = upre >= 0 && pick(pre, spre);
+                model.update_synapse(s, pb, pick(post, sp), st.dt);
+                sp = sp + 1 == HB ? 0u : sp + 1;
+                if (upre >= 0) spre = spre + 1 == HB ? 0u : spre + 1;
+                ++upre;
+            }
             store_syn_changed(st.sf, base + kk, s, s0);
         }
-        __syncwarp();
-        if (lane == 0) {
+        if (threadIdx.x == 0) {
             atomicAdd(&st.counters[C_SYN_UPDATES],
                       static_cast<unsigned long long>(d) * static_cast<unsigned long long>(through - a0 + 1));
             st.ages[nid] = static_cast<uint32_t>(through + 1);

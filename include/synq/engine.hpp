@@ -325,7 +325,8 @@ public:
         if constexpr (has_synapses) {
             push_mirrors();
             auto t0 = clock::now();
-            dev::k_catchup<Model><<<grid_for(uint64_t(n_) * 32, 256), 256, 0, stream_>>>(model_, state(), 1);
+            dev::k_catchup<Model><<<std::max<uint32_t>(1, std::min<uint32_t>(n_, uint32_t(sms_) * 8)), 256, 0, stream_>>>(
+                model_, state(), 1);
             SYNQ_CUDA(cudaGetLastError());
             pull_counters();
             timings_.simulate += since(t0);
@@ -1127,7 +1128,8 @@ private:
         auto st = state();
         dev::k_update<Model, kUpdateBlock><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
         if constexpr (has_synapses)
-            dev::k_catchup<Model><<<grid_for(uint64_t(n_) * 32, 256), 256, 0, stream_>>>(model_, st, 0);
+            dev::k_catchup<Model><<<std::max<uint32_t>(1, std::min<uint32_t>(n_, uint32_t(sms_) * 8)), 256, 0, stream_>>>(
+                model_, st, 0);
         const int rgrid = 8 * sms_;
         if (exact_) {
             dev::k_det_events<Model, kReceiveBlock, false><<<rgrid, kReceiveBlock, 0, stream_>>>(st);
