@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(NT, 1)
     __shared__ unsigned long long s_fval[MB][kMaxTiles];
     __shared__ uint32_t s_ok[MB];
     __shared__ uint32_t s_gbeg[32], s_gend[32];  // bitmap delivery: spike range of group frame * 4 + class
+    __shared__ uint32_t s_gcp[33];                // ... exclusive prefix of its 7-block chunks
     __shared__ uint32_t s_qbase[MB];  // queue slot base of frame w of the pass
     __shared__ uint32_t s_cbase[MB];  // count-ring slot base of frame w of the pass
     __shared__ uint32_t s_dtmp[DW + 1];
@@ -668,17 +669,33 @@ __global__ void __launch_bounds__(NT, 1)
                         if (i + 1 == n || s_grp[i + 1] != G) s_gend[G] = i + 1;
                     }
                     named_bar(BAR_D, DT);
-                    for (uint32_t u = dwarp; u < 32 * WQ; u += DW) {
-                        const uint32_t G = u >> wq_sh, q = u & (WQ - 1);
+                    // work items = (chunk of <= 7 blocks of one group, column):
+                    // groups differ ~5x in size, equal chunks keep the warps
+                    // balanced; chunks of one (group, column) add with
+                    // conflict-free shared atomics
+                    if (dwarp == 0) {
+                        const uint32_t gb = s_gbeg[lane], ge = s_gend[lane];
+                        const uint32_t nb = ge > gb ? ((ge + 31) >> 5) - (gb >> 5) : 0u;
+                        const uint32_t nc = (nb + 6) / 7;
+                        const uint32_t inc = warp_incl_scan(nc);
+                        s_gcp[lane] = inc - nc;
+                        if (lane == 31) s_gcp[32] = inc;
+                    }
+                    named_bar(BAR_D, DT);
+                    const uint32_t nwork = s_gcp[32] << wq_sh;
+                    for (uint32_t it = dwarp; it < nwork; it += DW) {
+                        const uint32_t q = it & (WQ - 1), ci = it >> wq_sh;
+                        uint32_t G = 0;  // last group with s_gcp[G] <= ci
+#pragma unroll
+                        for (uint32_t step = 16; step; step >>= 1)
+                            if (s_gcp[G + step] <= ci) G += step;
                         const uint32_t gb = s_gbeg[G], ge = s_gend[G];
-                        if (ge <= gb) continue;
+                        const uint32_t blk = (gb >> 5) + 7 * (ci - s_gcp[G]);
+                        const uint32_t take = min(7u, ((ge + 31) >> 5) - blk);
                         uint32_t cnt[4] = {0, 0, 0, 0};
-                        const uint32_t blk_end = (ge + 31) >> 5;
-                        uint32_t blk = gb >> 5;
-                        // >= 3 blocks: bit-sliced sum of up to 7 blocks per lane
-                        // (3 planes), then one transpose per plane
-                        while (blk + 3 <= blk_end) {
-                            const uint32_t take = min(7u, blk_end - blk);
+                        if (take >= 3) {
+                            // bit-sliced sum of the blocks per lane (3 planes),
+                            // then one transpose per plane
                             uint32_t p0[4] = {0, 0, 0, 0}, p1[4] = {0, 0, 0, 0}, p2[4] = {0, 0, 0, 0};
                             for (uint32_t v = 0; v < take; ++v) {
                                 const uint32_t gs = (blk + v) * 32 + lane;
@@ -696,32 +713,23 @@ __global__ void __launch_bounds__(NT, 1)
                             }
 #pragma unroll
                             for (int e = 0; e < 4; ++e)
-                                cnt[e] += __popc(transpose32(p0[e], tpk)) + (__popc(transpose32(p1[e], tpk)) << 1) +
-                                          (__popc(transpose32(p2[e], tpk)) << 2);
-                            blk += take;
-                        }
-                        for (; blk < blk_end; blk += 2) {
-                            uint4 x[2];
-                            unsigned m[2];
-#pragma unroll
-                            for (int v = 0; v < 2; ++v) {
-                                const uint32_t b0 = (blk + v) * 32, gs = b0 + lane;
+                                cnt[e] = __popc(transpose32(p0[e], tpk)) + (__popc(transpose32(p1[e], tpk)) << 1) +
+                                         (__popc(transpose32(p2[e], tpk)) << 2);
+                        } else {
+                            for (uint32_t v = 0; v < take; ++v) {
+                                const uint32_t gs = (blk + v) * 32 + lane;
                                 const bool in = gs >= gb && gs < ge;
-                                x[v] = in ? sw[gs * WQ + (q ^ ((gs >> swz_sh) & swz_m))] : make_uint4(0, 0, 0, 0);
-                                m[v] = __ballot_sync(0xffffffffu, in);
-                            }
-#pragma unroll
-                            for (int v = 0; v < 2; ++v) {
-                                cnt[0] += __popc(transpose32(x[v].x, tpk) & m[v]);
-                                cnt[1] += __popc(transpose32(x[v].y, tpk) & m[v]);
-                                cnt[2] += __popc(transpose32(x[v].z, tpk) & m[v]);
-                                cnt[3] += __popc(transpose32(x[v].w, tpk) & m[v]);
+                                const uint4 x = in ? sw[gs * WQ + (q ^ ((gs >> swz_sh) & swz_m))] : make_uint4(0, 0, 0, 0);
+                                cnt[0] += __popc(transpose32(x.x, tpk));
+                                cnt[1] += __popc(transpose32(x.y, tpk));
+                                cnt[2] += __popc(transpose32(x.z, tpk));
+                                cnt[3] += __popc(transpose32(x.w, tpk));
                             }
                         }
                         uint32_t* cb = ring + s_cbase[G >> 2] + (G & 3u) * ps.win_cap + q * 128 + lane;
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
-                            if (cnt[e]) cb[e * 32] += cnt[e];
+                            if (cnt[e]) atomicAdd(cb + e * 32, cnt[e]);
                         my_deliv += cnt[0] + cnt[1] + cnt[2] + cnt[3];
                     }
                     named_bar(BAR_D, DT);
