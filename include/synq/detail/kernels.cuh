@@ -530,21 +530,29 @@ __global__ void __launch_bounds__(BLOCK) k_det_apply(M model, engine_state<M> st
     step_epilogue(st, t);
 }
 
-// exclusive scan of det_cnt into det_off (single block, n-chunked; the
-// ordered path is the reference's deterministic mode, not the fast path)
+// exclusive scan of det_cnt into det_off (single block; each thread owns 16
+// consecutive counts per round, so a 45K-neuron network takes 3 rounds, not
+// 45; the ordered path is the reference's deterministic mode)
 template <class M, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_det_scan(engine_state<M> st) {
     const int64_t t = *st.t_dev;
     if (t - static_cast<int64_t>(st.delay) + 1 < 0) return;
+    constexpr uint32_t E = 16;  // counts per thread per round
     __shared__ uint32_t s_warp[BLOCK / 32];
     __shared__ uint32_t s_carry;
     if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    for (uint32_t base = 0; base < st.n; base += BLOCK) {
-        const uint32_t i = base + threadIdx.x;
-        const uint32_t c = i < st.n ? st.det_cnt[i] : 0;
-        uint32_t incl = c;
+    for (uint32_t base = 0; base < st.n; base += BLOCK * E) {
+        const uint32_t i0 = base + threadIdx.x * E;
+        uint32_t c[E];
+        uint32_t sum = 0;
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            c[e] = i0 + e < st.n ? st.det_cnt[i0 + e] : 0u;
+            sum += c[e];
+        }
+        uint32_t incl = sum;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= static_cast<uint32_t>(o)) incl += y;
@@ -561,7 +569,12 @@ __global__ void __launch_bounds__(BLOCK) k_det_scan(engine_state<M> st) {
             if (lane < BLOCK / 32) s_warp[lane] = wi - w;
         }
         __syncthreads();
-        if (i < st.n) st.det_off[i] = s_carry + s_warp[warp] + incl - c;
+        uint32_t run = s_carry + s_warp[warp] + incl - sum;
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            if (i0 + e < st.n) st.det_off[i0 + e] = run;
+            run += c[e];
+        }
         __syncthreads();
         if (threadIdx.x == BLOCK - 1) s_carry += s_warp[warp] + incl;
         __syncthreads();

@@ -540,10 +540,10 @@ public:
         m.neuron_fields = detail::field_bytes<neuron_fields>() * n_;
         m.neuron_rng = uses_rng ? uint64_t(n_) * sizeof(xorshift) : 0;
         m.spike_bitmasks = hist_.bytes();
-        m.spike_queues = queue_.bytes() + qcount_.bytes() + finfo_.bytes();
+        m.spike_queues = queue_.bytes() + qcount_.bytes() + finfo_.bytes() + xsend_.bytes() + xrecv_.bytes();
         m.ages = has_synapses ? uint64_t(n_) * 4 : 0;
         m.expirations = has_synapses ? uint64_t(n_) * 4 : 0;
-        m.adjacency = graph_.bytes() + split_.bytes();
+        m.adjacency = graph_.bytes() + split_.bytes() + bm_.bytes();  // + receive-window bitmaps
         m.synapse_fields = detail::field_bytes<synapse_fields>() * synapse_capacity();
         return m;
     }

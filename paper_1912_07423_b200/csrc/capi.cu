@@ -9,6 +9,7 @@
 #include <array>
 #include <cmath>
 #include <cstring>
+#include <thread>
 #include <fstream>
 #include <functional>
 #include <iostream>
@@ -796,9 +797,23 @@ synq_status synq_sim_raster_copy(const synq_sim* s, int64_t* steps, uint32_t* id
         set_error("raster buffers too small or null");
         return SYNQ_ERR_INVALID_ARGUMENT;
     }
-    for (size_t i = 0; i < r.size(); ++i) {
-        steps[i] = r[i].step;
-        ids[i] = r[i].neuron;
+    // large rasters are split into (steps, ids) by several host threads
+    auto part = [&](size_t a, size_t b) {
+        for (size_t i = a; i < b; ++i) {
+            steps[i] = r[i].step;
+            ids[i] = r[i].neuron;
+        }
+    };
+    const size_t n = r.size();
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    if (n < (size_t(1) << 18) || hw == 1) {
+        part(0, n);
+    } else {
+        std::vector<std::thread> pool;
+        const size_t per = (n + hw - 1) / hw;
+        for (unsigned k = 1; k < hw; ++k) pool.emplace_back(part, std::min(n, k * per), std::min(n, (k + 1) * per));
+        part(0, std::min(n, per));
+        for (auto& th : pool) th.join();
     }
     return SYNQ_OK;
 }
