@@ -190,6 +190,10 @@ __global__ void __launch_bounds__(NT, 1)
     // streamed update (NPT == 0): per (chunk, warp) spike counts and ballots
     constexpr int kSE = NPT == 0 ? kStreamChunks * UW : 1;
     __shared__ uint32_t s_sa[kSE], s_sb[kSE], s_spk[kSE];
+    // streamed bitmap delivery: frame table + linear work space
+    __shared__ uint32_t s_ft_base[MB], s_ft_nb[MB], s_ft_S[MB], s_ft_q[MB], s_ft_cb[MB], s_ft_done[MB];
+    __shared__ unsigned long long s_ft_lb[MB];
+    __shared__ uint32_t s_work_next, s_work_end, s_work_total;
     __shared__ uint32_t s_delivered;  // frames delivered: rel 0 .. s_delivered
     __shared__ uint32_t s_updated;    // update steps whose fold is done
     __shared__ unsigned long long s_prof[P_SLOTS];
@@ -207,6 +211,15 @@ __global__ void __launch_bounds__(NT, 1)
     if (tid == 0) {
         s_delivered = 0;
         s_updated = 0;
+        s_work_next = 0;
+        s_work_end = 0;
+        s_work_total = 0xffffffffu;
+    }
+    if (tid < MB) {
+        s_ft_base[tid] = 0;
+        s_ft_nb[tid] = 0;
+        s_ft_done[tid] = 0;
+        s_ft_S[tid] = 0;
     }
     __syncthreads();
     const uint32_t pa = ps.cta_piece[2 * c], pb = ps.cta_piece[2 * c + 1];
@@ -540,6 +553,146 @@ __global__ void __launch_bounds__(NT, 1)
         }
         if (tid == 0 && my_spikes) atomicAdd(&ps.counters[C_SPIKES], my_spikes);
         if (profiling) s_prof[P_STEPS] = static_cast<unsigned long long>(nsteps);
+    } else if (BM && ps.stream_mode) {
+        // ============================================ delivery warps (bitmap, streamed)
+        // No passes and no group barriers.  Warp 0 (poller) claims complete
+        // frames in order into a table of FT slots (piece prefix, queue /
+        // ring bases) and appends each frame's blocks of 32 spikes to a
+        // linear work space; the other warps take work items with one shared
+        // atomic and count each block independently: piece search, spike
+        // ids, receive windows straight into registers, warp bit-transposes,
+        // conflict-free shared atomics.  The poller releases frames in order
+        // once all their blocks are counted.
+        constexpr uint32_t FT = MB;
+        const uint32_t dwarp = warp - UW;
+        unsigned long long my_deliv = 0;
+        const bool log_cta = ps.log && c == 0;
+        const uint32_t WQ = ps.wq;
+        const tp_consts tpk = make_tp_consts(lane);
+        const uint4* bmw = ps.bm + static_cast<uint64_t>(c) * WQ;
+        uint32_t r_first = 1;
+        if (fbase + 1 < 0) r_first = static_cast<uint32_t>(min(-1 - fbase, static_cast<int64_t>(nrel))) + 1;
+        if (dwarp == 0) {
+            // ---------------- poller
+            if (r_first > 1 && lane == 0) st_release_cta(&s_delivered, r_first - 1);
+            uint32_t r_poll = r_first, r_rel = r_first, wend = 0;
+            unsigned long long lc = 0;
+            bool total_set = false;
+            while (r_rel <= nrel) {
+                bool progress = false;
+                // release counted frames in order
+                while (r_rel < r_poll) {
+                    const uint32_t sl = r_rel % FT;
+                    if (ld_acquire_cta(&s_ft_done[sl]) != s_ft_nb[sl]) break;
+                    if (lane == 0) st_release_cta(&s_delivered, r_rel);
+                    ++r_rel;
+                    progress = true;
+                }
+                // claim the next frame when it is complete and its ring slot free
+                if (r_poll <= nrel && r_poll < r_rel + FT && r_poll + 1 <= ld_acquire_cta(&s_updated) + R &&
+                    (ps.lag == 0 || frame_complete(ps, fbase + r_poll + ps.lag, false, ps.C))) {
+                    const uint32_t sl = r_poll % FT;
+                    if (frame_prefix(ps, fbase + r_poll, s_seg[sl], s_fval[0], s_psrc, true)) {
+                        const uint32_t S = s_seg[sl][P], nb = (S + 31) / 32;
+                        const bool logged = log_cta && fbase + r_poll >= ps.log_from;
+                        if (lane == 0) {
+                            s_ft_base[sl] = wend;
+                            s_ft_nb[sl] = nb;
+                            s_ft_S[sl] = S;
+                            s_ft_q[sl] = static_cast<uint32_t>((fbase + r_poll) % ps.Q) * ps.n;
+                            s_ft_cb[sl] = (r_poll % R) * ps.K * ps.win_cap;
+                            s_ft_lb[sl] = logged ? lc : ~0ull;
+                            s_ft_done[sl] = 0;
+                        }
+                        if (logged) lc += S;
+                        wend += nb;
+                        __syncwarp();
+                        if (lane == 0) st_release_cta(&s_work_end, wend);
+                        ++r_poll;
+                        progress = true;
+                    }
+                }
+                if (r_poll > nrel && !total_set) {
+                    if (lane == 0) st_release_cta(&s_work_total, wend);
+                    total_set = true;
+                }
+                if (!progress) __nanosleep(32);
+            }
+            if (!total_set && lane == 0) st_release_cta(&s_work_total, wend);
+            if (log_cta && lane == 0) {
+                *ps.log_end = lc;
+                if (lc > ps.log_cap) ps.flags[0] = 1;
+            }
+        } else {
+            // ---------------- workers
+            for (;;) {
+                uint32_t item = 0;
+                if (lane == 0) item = atomicAdd(&s_work_next, 1u);
+                item = __shfl_sync(0xffffffffu, item, 0);
+                bool done = false;
+                for (;;) {  // wait until the item exists (or the launch has no more work)
+                    if (item < ld_acquire_cta(&s_work_end)) break;
+                    if (item >= ld_acquire_cta(&s_work_total)) {
+                        done = true;
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+                if (done) break;
+                uint32_t sl = 0;
+#pragma unroll
+                for (uint32_t k = 0; k < FT; ++k) {
+                    const uint32_t b0 = s_ft_base[k];
+                    if (item >= b0 && item < b0 + s_ft_nb[k] && s_ft_done[k] < s_ft_nb[k]) sl = k;
+                }
+                const uint32_t S = s_ft_S[sl], blk = item - s_ft_base[sl];
+                const uint32_t* seg = s_seg[sl];
+                const uint32_t g = blk * 32 + lane;
+                const bool valid = g < S;
+                uint32_t src = 0, cls = 0xffu;
+                if (valid) {
+                    const uint32_t a = piece_of(seg, P, g);
+                    src = __ldcg(ps.queue + s_ft_q[sl] + s_lo[a] + (g - seg[a]));
+                    cls = static_cast<uint32_t>(source_class(ps, src));
+                    const unsigned long long lb = s_ft_lb[sl];
+                    if (lb != ~0ull && lb + g < ps.log_cap) ps.log[lb + g] = src;
+                }
+                unsigned cm[kMaxClasses];
+#pragma unroll
+                for (int k = 0; k < kMaxClasses; ++k) cm[k] = __ballot_sync(0xffffffffu, cls == static_cast<uint32_t>(k));
+                uint32_t* rb = ring + s_ft_cb[sl] + lane;
+                const uint4* row = bmw + static_cast<uint64_t>(src) * ps.bm_row4;
+                for (uint32_t q0 = 0; q0 < WQ; q0 += 4) {
+                    uint4 x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        x[u] = (valid && q0 + u < WQ) ? ldg_stream4(row + q0 + u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (q0 + u >= WQ) break;
+                        const uint32_t wv[4] = {transpose32(x[u].x, tpk), transpose32(x[u].y, tpk),
+                                                transpose32(x[u].z, tpk), transpose32(x[u].w, tpk)};
+#pragma unroll
+                        for (int k = 0; k < kMaxClasses; ++k) {
+                            if (!cm[k]) continue;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const uint32_t cnt = __popc(wv[e] & cm[k]);
+                                if (cnt) {
+                                    atomicAdd(rb + k * ps.win_cap + ((q0 + u) * 4 + e) * 32, cnt);
+                                    my_deliv += cnt;
+                                }
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                __threadfence_block();
+                if (lane == 0) atomicAdd(&s_ft_done[sl], 1u);
+            }
+        }
+        for (int o = 16; o; o >>= 1) my_deliv += __shfl_xor_sync(0xffffffffu, my_deliv, o);
+        if (lane == 0 && my_deliv) atomicAdd(&ps.counters[C_DELIVERIES], my_deliv);
     } else {
         // ============================================ delivery warps
         const uint32_t dtid = tid - UT, dwarp = warp - UW;

@@ -1116,6 +1116,8 @@ private:
         p.bm_row4 = bm_row4_;
         p.wq = bm_wq_;
         p.bm_prefetch = pipe_bm_ && lag_ > 0 ? 1u : 0u;
+        p.stream_mode = 0;
+        if (const char* e = std::getenv("SYNQ_WORKQ")) p.stream_mode = std::atoi(e) != 0 ? 1u : 0u;
         return p;
     }
 

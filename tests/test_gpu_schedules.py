@@ -25,7 +25,7 @@ pytestmark = pytest.mark.gpu
 
 
 def build(m, env, monkeypatch, **kw):
-    for k in ("SYNQ_BITMAP", "SYNQ_UW", "SYNQ_LAG", "SYNQ_LEAD", "SYNQ_PREFETCH", "SYNQ_STREAM"):
+    for k in ("SYNQ_BITMAP", "SYNQ_UW", "SYNQ_LAG", "SYNQ_LEAD", "SYNQ_PREFETCH", "SYNQ_STREAM", "SYNQ_WORKQ"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, str(v))
@@ -127,5 +127,19 @@ def test_streamed_state(golden, monkeypatch, tag, bitmap):
     sweep networks), forced on the golden networks."""
     sim = build(golden["meta"]["runs"][tag], {"SYNQ_STREAM": 1, "SYNQ_BITMAP": bitmap}, monkeypatch, pipeline=1)
     assert sim.pipelined
+    check(sim, golden, tag)
+    sim.close()
+
+
+@pytest.mark.parametrize("tag", ["brunel_20000_s1_t2000_h0_d0", "brunel_2000_s99_t3000_h0_d0",
+                                 "vogels_1000_s99_t3000_h0_d0"])
+@pytest.mark.parametrize("uw", [4, 16])
+def test_workqueue_delivery(golden, monkeypatch, tag, uw):
+    """Barrier-free bitmap delivery (SYNQ_WORKQ=1: a poller warp claims
+    frames, worker warps take 32-spike blocks from a linear work space) —
+    experimental schedule, must be bit-exact like every other."""
+    sim = build(golden["meta"]["runs"][tag], {"SYNQ_WORKQ": 1, "SYNQ_BITMAP": 2, "SYNQ_UW": uw}, monkeypatch,
+                pipeline=1)
+    assert sim.engine == "pipelined-bitmap"
     check(sim, golden, tag)
     sim.close()
