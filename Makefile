@@ -47,7 +47,7 @@ LIB_OBJS := $(OBJDIR)/capi.o $(OBJDIR)/construct.o $(OBJDIR)/host_model.o $(OBJD
 
 $(LIBDIR)/libsynq.so.1: $(LIB_OBJS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -Xlinker -soname,libsynq.so.1 -o $@ $(LIB_OBJS) -lcudart -lnccl
+	$(NVCC) $(ARCH) -shared -Xlinker -soname,libsynq.so.1 -o $@ $(LIB_OBJS) -lcudart -ldl
 	ln -sf libsynq.so.1 $(LIBDIR)/libsynq.so
 
 oracle:

@@ -368,7 +368,9 @@ public:
     unsigned tiles() const { return tiles_; }
 
     // ---- multi-GPU shard exchange -------------------------
-    bool sharded() const { return opt_.shard_world > 1; }
+    // a shard of a multi-GPU run; an in-engine NCCL exchange is a shard even
+    // with one rank (then the allgather copies the rank's own block)
+    bool sharded() const { return opt_.shard_world > 1 || opt_.shard_nccl; }
     // words needed to export the frames of the last run() (upper bound)
     uint64_t export_capacity() const {
         return 1 + 2ull * (delay_ ? delay_ : 1) + uint64_t(delay_) * ((shard_lo_[1] - shard_lo_[0]) + (shard_lo_[3] - shard_lo_[2]));

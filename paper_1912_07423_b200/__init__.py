@@ -195,6 +195,7 @@ class Opts:
         if shard is not None:
             check(L.synq_opts_shard(self.h, int(shard[0]), int(shard[1])))
         if shard_nccl is not None:  # (rank, world, 128-byte NCCL unique id)
+            _prefer_torch_nccl()
             rank, world, uid = shard_nccl
             buf = C.create_string_buffer(bytes(uid), 128)
             check(L.synq_opts_shard_nccl(self.h, int(rank), int(world), buf))
@@ -441,9 +442,20 @@ class Sim:
         return int(out[0]), int(out[1])
 
 
+def _prefer_torch_nccl():
+    """libsynq opens NCCL on first use and reuses a libnccl.so.2 already in the
+    process: load torch's (newer) one first when torch is installed, so both
+    share it."""
+    try:
+        import torch  # noqa: F401
+    except Exception:
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """A fresh 128-byte NCCL unique id for synq_opts_shard_nccl (make it on one
     rank and broadcast it)."""
+    _prefer_torch_nccl()
     buf = C.create_string_buffer(128)
     check(lib().synq_nccl_unique_id(buf))
     return buf.raw

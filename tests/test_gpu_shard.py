@@ -150,3 +150,25 @@ def test_sharded_processes_gloo(golden):
             parts.append((((rg[0], rg[1]), (rg[2], rg[3])), z["v"]))
         v = shard.assemble_field(parts)
         assert np.array_equal(v.view(np.uint32), runs[f"{tag}_f0"])
+
+
+def test_nccl_in_engine_single_rank(golden):
+    """The in-engine exchange end to end on one GPU: a one-rank NCCL
+    communicator, export -> ncclAllGather -> import on the engine stream after
+    every batch of delay-1 steps, recording through the shard's own frame
+    log.  Frames, state and counters stay bit-exact with the reference."""
+    runs = golden["runs"]
+    for tag, m in population_runs(golden):
+        uid = synq.nccl_unique_id()
+        opts = synq.Opts(seed=m["seed"], deterministic=True, record=True, dt=m["dt"] or None,
+                         delay=m["delay"] or None, shard_nccl=(0, 1, uid))
+        sim = synq.Sim(m["model"], m["neurons"], opts)
+        assert sim.persistent and sim.shard_capacity() > 0
+        sim.run(m["steps"])  # any number of steps: the engine exchanges internally
+        counts, ids = sim.frames()
+        assert np.array_equal(counts, runs[f"{tag}_counts"]), tag
+        assert np.array_equal(ids, runs[f"{tag}_ids"]), tag
+        for i in range(3):
+            assert np.array_equal(sim.neuron_field(i).view(np.uint32), runs[f"{tag}_f{i}"]), (tag, i)
+        assert sim.counters()["deliveries"] == m["counters"]["deliveries"], tag
+        sim.close()
