@@ -1,0 +1,18 @@
+"""Per-GPU cost of the in-engine NCCL shard loop on one B200: Brunel 1e9 as
+a one-rank NCCL shard (14-step launches + export_bits + ncclAllGather +
+import per batch) vs the unsharded engine (1000-step launches)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1912_07423_b200 as synq
+
+for name, kw in (("unsharded", {}), ("nccl shard (1 rank)", {"shard_nccl": (0, 1, synq.nccl_unique_id())})):
+    sim = synq.Sim("brunel", opts=synq.Opts(seed=1, deterministic=True, **kw), synapses=int(1e9))
+    sim.run(2000)
+    d0, k0 = sim.device_time()
+    sim.run(10000)
+    d1, k1 = sim.device_time()
+    print(f"{name:22s}: {(d1 - d0) * 1e3:.1f} ms per bio-s device ({(k1 - k0) * 1e3:.1f} ms in step kernels), "
+          f"launches {sim.kernel_launches()}", flush=True)
+    sim.close()
