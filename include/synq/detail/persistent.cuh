@@ -98,6 +98,7 @@ struct persist_state {
     uint32_t wq;           // uint4 per window (1, 2, 4 or 8)
     uint32_t bm_prefetch;  // stream the bitmap rows of published spikes into L2
     uint32_t stream_mode;  // bitmap delivery: barrier-free work items instead of passes
+    uint32_t max_pass;     // frames per delivery pass (<= the polling warps)
 };
 
 // streaming 16-byte read of adjacency cells: read-only, no L1 allocation

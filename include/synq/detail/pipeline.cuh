@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(NT, 1)
             fpre[0] = 0;
 #pragma unroll
             for (int w = 0; w < MB; ++w) {
-                const bool take = (static_cast<uint32_t>(w) == B) && s_ok[w];
+                const bool take = (static_cast<uint32_t>(w) == B) && s_ok[w] && static_cast<uint32_t>(w) < ps.max_pass;
                 if (take) ++B;
                 fpre[w + 1] = fpre[w] + (take ? s_seg[w][P] : 0u);
             }
