@@ -646,9 +646,13 @@ private:
         const uint32_t nr = r1 - r0;
         const uint32_t NTH = dev::kPersistThreads;
         // ~90% thread occupancy per CTA keeps one neuron per thread (NPT = 1)
+        // about one CTA per 128 neurons, up to one per SM: the pipelined
+        // kernel's delivery work per step does not shrink with the neurons a
+        // CTA owns, so a shard of a multi-GPU run still uses every SM
+        constexpr int64_t kNeuronsPerTile = 128;
         uint32_t C = opt_.tiles ? opt_.tiles
                                 : static_cast<uint32_t>(std::clamp<int64_t>(
-                                      (static_cast<int64_t>(n_) * 10 + 9 * NTH - 1) / (9 * NTH), 1, sms_));
+                                      (static_cast<int64_t>(n_) + kNeuronsPerTile - 1) / kNeuronsPerTile, 1, sms_));
         C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), n_});
         const uint32_t max_local = 4 * NTH;  // register-resident state: <= 4 neurons per thread
         if (uint64_t(C) * max_local < n_) C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (n_ + max_local - 1) / max_local));
@@ -681,7 +685,7 @@ private:
         if (W > 1) {  // the local shard sizes its CTA count by its own neurons
             const uint64_t mine = (ra[R + 1] - ra[R]) + (ub[R + 1] - ub[R]);
             if (!opt_.tiles)
-                C = static_cast<uint32_t>(std::clamp<int64_t>((static_cast<int64_t>(mine) * 10 + 9 * NTH - 1) / (9 * NTH), 1, sms_));
+                C = static_cast<uint32_t>(std::clamp<int64_t>((static_cast<int64_t>(mine) + kNeuronsPerTile - 1) / kNeuronsPerTile, 1, sms_));
         }
         if (C + W - 1 > uint32_t(dev::kMaxTiles)) return;
         if (2ull * delay_ >= (1u << 15)) return;  // 16-bit frame tags need Q << 65536
