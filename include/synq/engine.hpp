@@ -819,7 +819,7 @@ private:
 
     // this shard's frames of steps [t0, t0+b) -> its bitmask block at `out`
     void enqueue_export_bits(int64_t t0, uint32_t b, uint32_t* out) requires population_model {
-        dev::k_export_bits<Model><<<std::max<uint32_t>(1, b), 256, (xl_.wa + xl_.wb) * 4, stream_>>>(
+        dev::k_export_bits<Model><<<std::max<uint32_t>(1, b), 1024, (xl_.wa + xl_.wb) * 4, stream_>>>(
             pstate(), t0, b, xl_, shard_lo_[0], shard_lo_[2], out);
         SYNQ_CUDA(cudaGetLastError());
         launches_ += 1;

@@ -6,7 +6,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1912_07423_b200 as synq
 
-for b in (1000, 100, 14, 7):
+for b in [int(x) for x in os.environ.get('BATCHES', '1000,100,14,7').split(',')]:
     sim = synq.Sim("brunel", opts=synq.Opts(seed=1, deterministic=True, batch_steps=b), synapses=int(1e9))
     sim.run(2000)
     d0, k0 = sim.device_time()
