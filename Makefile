@@ -43,7 +43,7 @@ $(OBJDIR)/%.o: $(PKG)/csrc/%.cpp $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-LIB_OBJS := $(OBJDIR)/capi.o $(OBJDIR)/construct.o $(OBJDIR)/host_model.o $(OBJDIR)/nccl_glue.o
+LIB_OBJS := $(OBJDIR)/capi.o $(OBJDIR)/construct.o $(OBJDIR)/plan.o $(OBJDIR)/host_model.o $(OBJDIR)/nccl_glue.o
 
 $(LIBDIR)/libsynq.so.1: $(LIB_OBJS)
 	@mkdir -p $(LIBDIR)

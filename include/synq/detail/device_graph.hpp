@@ -30,7 +30,11 @@ struct device_graph {
     uint64_t bytes() const { return cells.bytes() + degree.bytes(); }
 };
 
-// plan on the host (bit-exact, sequential master stream), expand on the device
+// the degree plan of plan_jobs drawn on the device (csrc/plan.cu); the same
+// construction_plan as the host plan_jobs, bit for bit
+construction_plan plan_jobs_device(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
+                                   cudaStream_t stream);
+// plan on the device (SYNQ_HOST_PLAN=1: on the host), expand on the device
 device_graph build_device_graph(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
                                 cudaStream_t stream);
 device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons, uint64_t seed,

@@ -4,9 +4,10 @@
 // build_adjacency) and proj/include/synq/adjacency.hpp:112-163
 // (sorted_random).
 //
-// * plan_jobs stays on the host: it is ONE sequential binomial stream
-//   (derive_seed(seed, 0)) whose draw positions are data dependent, and glibc
-//   log/log1p decide the degrees, so the host reproduces it bit for bit.
+// * plan_jobs: ONE sequential binomial stream (derive_seed(seed, 0)) whose
+//   draw positions are data dependent.  The host restatement below is kept as
+//   the SYNQ_HOST_PLAN=1 path and the check; the default is the device plan
+//   (csrc/plan.cu): the same stream jumped ahead per thread, glibc-guarded.
 // * expansion runs on the device, one thread per job.  Each thread replays
 //   its job's xorshift stream twice (pass 1: the exclusive-sum total, pass 2:
 //   the outputs) with the same left-to-right double summation as the
@@ -22,6 +23,7 @@
 //   reference's.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <numeric>
@@ -321,8 +323,11 @@ device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons
 
 device_graph build_device_graph(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
                                 cudaStream_t stream) {
-    return expand_device_graph(plan_jobs(desc, seed, pitch_align), desc.neuron_count(), seed,
-                               stream);
+    const char* host = std::getenv("SYNQ_HOST_PLAN");
+    const bool on_host = host && std::atoi(host) != 0;
+    return expand_device_graph(on_host ? plan_jobs(desc, seed, pitch_align)
+                                       : plan_jobs_device(desc, seed, pitch_align, stream),
+                               desc.neuron_count(), seed, stream);
 }
 
 adjacency_list download_graph(const device_graph& g, cudaStream_t stream) {

@@ -10,6 +10,9 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+
+#include "synq/detail/device_graph.hpp"
 #include "synq/engine.hpp"
 #include "synq/models/benchmarks.hpp"
 
@@ -357,6 +360,59 @@ void test_accumulation_modes() {
     }
 }
 
+// The device degree plan (csrc/plan.cu) against the host restatement of
+// plan_jobs (adjacency.cpp:29-71): every job, degree and offset identical.
+static network_desc make_desc(std::vector<uint32_t> pops, std::vector<connectivity_spec> conns) {
+    network_desc d;
+    for (uint32_t n : pops) d.populations.push_back(population_spec{n});
+    d.connections = std::move(conns);
+    d.dt = 0.1;
+    d.delay = 2;
+    return d;
+}
+
+static void check_plan(const network_desc& d, uint64_t seed, const char* name) {
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    const construction_plan a = plan_jobs(d, seed, 32);
+    const auto t1 = clk::now();
+    const construction_plan b = plan_jobs_device(d, seed, 32, nullptr);
+    const auto t2 = clk::now();
+    CHECK(a.jobs.size() == b.jobs.size());
+    size_t bad = 0;
+    for (size_t q = 0; q < std::min(a.jobs.size(), b.jobs.size()); ++q) {
+        const auto &x = a.jobs[q], &y = b.jobs[q];
+        bad += x.n != y.n || x.a != y.a || x.b != y.b || x.o != y.o;
+    }
+    CHECK(bad == 0);
+    CHECK(a.out_degree == b.out_degree);
+    CHECK(a.deg_max == b.deg_max);
+    CHECK(a.row_pitch == b.row_pitch);
+    CHECK(a.total_edges == b.total_edges);
+    std::printf("  plan %-10s seed %llu: %zu jobs, %llu edges, host %.3f s, device %.3f s, mismatched jobs %zu\n", name,
+                static_cast<unsigned long long>(seed), a.jobs.size(), static_cast<unsigned long long>(a.total_edges),
+                std::chrono::duration<double>(t1 - t0).count(), std::chrono::duration<double>(t2 - t1).count(), bad);
+}
+
+void test_plan() {
+    // Vogels 4000 and a small Brunel shape
+    check_plan(make_desc({3200, 800}, {{0, 0, 0.02}, {0, 1, 0.02}, {1, 0, 0.02}, {1, 1, 0.02}}), 1, "vogels4k");
+    check_plan(make_desc({5657, 1414, 7071}, {{0, 0, 0.1}, {0, 1, 0.1}, {1, 0, 0.1}, {1, 1, 0.1}, {2, 0, 0.1}, {2, 1, 0.1}}),
+               7, "brunel1e7");
+    // edge cases: p = 0 and p = 1 (no draws), sparse and dense, a one-neuron
+    // population, mixed p across connections
+    check_plan(make_desc({1, 300000, 2000, 37},
+                         {{0, 1, 0.001}, {1, 2, 0.0}, {2, 3, 1.0}, {1, 0, 0.5}, {3, 1, 0.0001}, {2, 2, 0.9}, {3, 3, 0.3}}),
+               12345, "edge");
+    for (uint64_t seed : {2ull, 3ull}) check_plan(make_desc({20000, 30000}, {{0, 1, 0.05}, {1, 0, 0.2}}), seed, "two-pop");
+}
+
+void test_plan_large() {
+    // Brunel 1e9 (282,842 jobs, 999,981,220 edges)
+    check_plan(make_desc({56568, 14142, 70711}, {{0, 0, 0.1}, {0, 1, 0.1}, {1, 0, 0.1}, {1, 1, 0.1}, {2, 0, 0.1}, {2, 1, 0.1}}),
+               1, "brunel1e9");
+}
+
 int main(int argc, char** argv) {
     const std::string only = argc > 1 ? argv[1] : "";
     auto run = [&](const char* name, void (*fn)()) {
@@ -369,6 +425,8 @@ int main(int argc, char** argv) {
     run("reinit", test_reinit);
     run("span_writeback", test_span_writeback);
     run("accumulation_modes", test_accumulation_modes);
+    run("plan", test_plan);
+    if (only == "plan_large") test_plan_large();
     if (only.empty() || only == "lazy") {
         check_lazy_equals_eager(120, 400, 0, 2024);
         check_lazy_equals_eager(80, 200, 1, 7);
