@@ -20,12 +20,17 @@ HDRS     := $(wildcard include/synq/*.hpp include/synq/*.h include/synq/models/*
 all: lib oracle tests
 
 # C++ model-API tests (device engine with user models), run by tests/test_gpu_cpp.py
-tests: build/test_network build/sweep
+tests: build/test_network build/sweep build/synq
 
 build/test_network: tests/cpp/test_network.cu $(HDRS) $(LIBDIR)/libsynq.so.1
 	@mkdir -p build
 	$(NVCC) -std=c++20 -O2 $(ARCH) -lineinfo -fmad=false --expt-relaxed-constexpr -Iinclude \
 	    -o $@ $< -L$(LIBDIR) -lsynq -Xlinker -rpath,'$$ORIGIN/../$(LIBDIR)'
+
+# command line front end over the C ABI (tools/cli/synq.cpp)
+build/synq: tools/cli/synq.cpp include/synq/synq.h $(LIBDIR)/libsynq.so.1
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lsynq -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
 
 # synthetic connectivity x rate sweep through the C++ model API (tools/sweep)
 build/sweep: tools/sweep/sweep.cu $(HDRS) $(LIBDIR)/libsynq.so.1

@@ -25,7 +25,9 @@
 //   (an unfinished job is redone from its first draw in the next round) and
 //   assembles the same construction_plan as plan_jobs.  Bit-identical to the
 //   host plan by construction; tests/cpp/test_network.cu (case plan) checks it.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -258,6 +260,7 @@ __global__ void k_plan_walk(const uint32_t* __restrict__ h, const unsigned long 
 
 construction_plan plan_jobs_device(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
                                    cudaStream_t stream) {
+    const auto t_begin = std::chrono::steady_clock::now();
     static const jump_table jt;
     construction_plan plan;
     const uint32_t n = desc.neuron_count();
@@ -287,6 +290,16 @@ construction_plan plan_jobs_device(const network_desc& desc, uint64_t seed, uint
     master.save(state);
     std::vector<uint32_t> hits;
     std::vector<uint2> fl;
+    const char* prof_env = std::getenv("SYNQ_PLAN_PROFILE");
+    const bool prof = prof_env && std::atoi(prof_env) != 0;
+    double t_draw = 0, t_walk = 0, t_pre = 0, t_conn = 0;
+    {
+        SYNQ_CUDA(cudaStreamSynchronize(stream));
+        t_pre = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count();
+    }
+    const auto t_loop = std::chrono::steady_clock::now();
+    uint64_t rounds = 0, guarded = 0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
 
     for (const auto& c : desc.connections) {
         auto [sa, sb] = desc.id_range(c.src);
@@ -311,6 +324,7 @@ construction_plan plan_jobs_device(const network_desc& desc, uint64_t seed, uint
                     h.resize(draws);
                     bsum.resize(draws / kBlock);
                 }
+                const auto tp0 = now();
                 nflags.zero(stream);
                 k_plan_draws<<<(threads + 255) / 256, 256, 0, stream>>>(
                     djump.get(), make_uint4(state[0], state[1], state[2], state[3]), threads, denom, cap, h.get(),
@@ -319,6 +333,10 @@ construction_plan plan_jobs_device(const network_desc& desc, uint64_t seed, uint
                 unsigned nf = 0;
                 nflags.download(&nf, 1, stream);
                 SYNQ_CUDA(cudaStreamSynchronize(stream));
+                const auto tp1 = now();
+                t_draw += std::chrono::duration<double>(tp1 - tp0).count();
+                ++rounds;
+                guarded += nf;
                 if (nf > kFlagCap) throw std::runtime_error("plan: too many rounding-guard draws");
                 if (nf) {
                     // the reference's own arithmetic (geometric, random.hpp:69-72)
@@ -340,6 +358,7 @@ construction_plan plan_jobs_device(const network_desc& desc, uint64_t seed, uint
                 unsigned long long res[2];
                 result.download(res, 2, stream);
                 SYNQ_CUDA(cudaStreamSynchronize(stream));
+                t_walk += std::chrono::duration<double>(now() - tp1).count();
                 if (res[0] == 0) {
                     if (threads == kPlanMaxThreads) throw std::runtime_error("plan: job longer than a round");
                     grow *= 4.0;
@@ -358,6 +377,13 @@ construction_plan plan_jobs_device(const network_desc& desc, uint64_t seed, uint
             plan.jobs[first[s] + filled[s]++] = construction_job{k, ta, tb, 0};
         }
     }
+    t_conn = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_loop).count();
+    if (prof)
+        std::fprintf(stderr,
+                     "plan_jobs_device: setup %.3f s, connections %.3f s (%llu rounds, draws %.3f s, walk %.3f s), "
+                     "%llu guarded draws\n",
+                     t_pre, t_conn, static_cast<unsigned long long>(rounds), t_draw, t_walk,
+                     static_cast<unsigned long long>(guarded));
     for (uint32_t d : plan.out_degree) plan.deg_max = std::max(plan.deg_max, d);
     if (pitch_align == 0) pitch_align = 1;
     plan.row_pitch = (plan.deg_max + pitch_align - 1) / pitch_align * pitch_align;

@@ -373,6 +373,7 @@ static network_desc make_desc(std::vector<uint32_t> pops, std::vector<connectivi
 
 static void check_plan(const network_desc& d, uint64_t seed, const char* name) {
     using clk = std::chrono::steady_clock;
+    cudaFree(nullptr);  // context creation is not part of the plan
     const auto t0 = clk::now();
     const construction_plan a = plan_jobs(d, seed, 32);
     const auto t1 = clk::now();
