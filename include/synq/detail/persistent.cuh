@@ -751,18 +751,18 @@ __global__ void k_export_bits(persist_state<M> ps, int64_t t0, uint32_t b, xbits
     const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
     const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(slot) * ps.E;
     const uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (uint32_t c = warp; c < ps.C; c += nw) {  // warp per local CTA
+    // thread per (local CTA, part): a frame holds a few ids per CTA, so one
+    // round of independent load chains (finfo, piece offset, ids) covers all
+    for (uint32_t x = threadIdx.x; x < 2 * ps.C; x += blockDim.x) {
+        const uint32_t c = x >> 1, part = x & 1;
+        const uint32_t lo = ps.piece_lo[ps.cta_piece[2 * c + part]];
         const unsigned long long e = fi[c];
-        const uint32_t ca = word_a(e), cb = word_b(e);
-        const uint32_t alo = ps.piece_lo[ps.cta_piece[2 * c]], blo = ps.piece_lo[ps.cta_piece[2 * c + 1]];
-        for (uint32_t j = lane; j < ca; j += 32) {
-            const uint32_t i = q[alo + j] - a_lo;
-            atomicOr(&s_bits[i >> 5], 1u << (i & 31));
-        }
-        for (uint32_t j = lane; j < cb; j += 32) {
-            const uint32_t i = q[blo + j] - b_lo;
-            atomicOr(&s_bits[L.wa + (i >> 5)], 1u << (i & 31));
+        const uint32_t cnt = part ? word_b(e) : word_a(e);
+        const uint32_t base = part ? b_lo : a_lo, woff = part ? L.wa : 0u;
+#pragma unroll 4
+        for (uint32_t j = 0; j < cnt; ++j) {
+            const uint32_t i = q[lo + j] - base;
+            atomicOr(&s_bits[woff + (i >> 5)], 1u << (i & 31));
         }
     }
     __syncthreads();
