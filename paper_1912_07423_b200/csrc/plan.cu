@@ -214,6 +214,10 @@ __global__ void k_plan_walk(const uint32_t* __restrict__ h, const unsigned long 
     uint32_t done = 0;
     uint32_t v[8];
     uint64_t cached = ~0ull;
+    // block-sum window prefetched with the block a job ends in: the next
+    // job starts there, so its window (blocks pf_base ..) is already loaded
+    unsigned long long pf = 0;
+    uint64_t pf_base = ~0ull;
     while (done < jobs) {
         unsigned long long need = target;
         uint64_t blk = start / kBlock;
@@ -228,7 +232,8 @@ __global__ void k_plan_walk(const uint32_t* __restrict__ h, const unsigned long 
             // skip whole blocks with the block sums, 32 at a time
             ++blk;
             if (blk >= nblocks) break;
-            const unsigned long long bs = blk + lane < nblocks ? bsum[blk + lane] : 0ull;
+            const unsigned long long bs =
+                blk == pf_base ? pf : (blk + lane < nblocks ? bsum[blk + lane] : 0ull);
             const unsigned long long incl = warp_incl_u64(bs, lane);
             const unsigned hit = __ballot_sync(0xffffffffu, incl >= need);
             if (!hit) {
@@ -240,6 +245,8 @@ __global__ void k_plan_walk(const uint32_t* __restrict__ h, const unsigned long 
             need -= __shfl_sync(0xffffffffu, incl - bs, fl);
             blk += fl;
             load_block(h, blk, lane, v);
+            pf_base = blk + 1;
+            pf = pf_base + lane < nblocks ? bsum[pf_base + lane] : 0ull;
             cached = blk;
             at = find_in_block(v, 0, need, lane);
             ok = true;  // the block sum says it ends here
