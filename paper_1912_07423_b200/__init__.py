@@ -162,7 +162,8 @@ class Opts:
                  record=None, defaults_file=None, params=None, batch_steps=None,
                  persistent=None, tiles=None, profile=None, shard=None, pipeline=None, lead=0,
                  shard_nccl=None):
-        self.h = lib().synq_opts_new()
+        self._L = lib()  # kept: module globals may be gone when __del__ runs at exit
+        self.h = self._L.synq_opts_new()
         if not self.h:
             raise MemoryError("synq_opts_new")
         L = lib()
@@ -202,7 +203,7 @@ class Opts:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().synq_opts_free(self.h)
+            self._L.synq_opts_free(self.h)
             self.h = None
 
 
@@ -220,12 +221,13 @@ class Sim:
             check(L.synq_sim_new_for_synapses(model.encode(), synapses, o, C.byref(h)))
         else:
             check(L.synq_sim_new(model.encode(), neurons, o, C.byref(h)))
+        self._L = lib()
         self.h = h
         self._opts = opts
 
     def close(self):
         if getattr(self, "h", None):
-            lib().synq_sim_free(self.h)
+            self._L.synq_sim_free(self.h)
             self.h = None
 
     def __del__(self):

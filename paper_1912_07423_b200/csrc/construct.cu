@@ -23,6 +23,7 @@
 //   reference's.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -307,6 +308,9 @@ device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons
         fl.resize(jobs.size());
         std::iota(fl.begin(), fl.end(), 0);
     }
+    const char* prof_env = std::getenv("SYNQ_PLAN_PROFILE");
+    if (prof_env && std::atoi(prof_env) != 0)
+        std::fprintf(stderr, "expand: %zu jobs recomputed on the host\n", fl.size());
     std::vector<uint32_t> buf;
     for (uint64_t j : fl) {
         const dev_job& job = jobs[j];
