@@ -612,6 +612,7 @@ private:
         batch_cap_ = opt_.batch_steps ? opt_.batch_steps : 1000;
         step_spikes_dev_.resize(2 * size_t(batch_cap_));
         step_meas_dev_.resize(2 * size_t(batch_cap_));
+        step_ctr_dev_.resize(4 * size_t(batch_cap_));
         step_buf_.resize(4 * size_t(batch_cap_));
     }
 
@@ -1250,8 +1251,10 @@ private:
     void launch_persistent(uint32_t b, int slot) {
         if constexpr (population_model) {
             auto ps = pstate();
-            ps.step_spikes = step_spikes_dev_.get() + size_t(slot) * batch_cap_;
-            ps.step_meas = step_meas_dev_.get() + size_t(slot) * batch_cap_;
+            // one counter block per slot: spikes [0, cap), measured [cap, cap + b),
+            // so a batch costs one memset and one copy
+            ps.step_spikes = step_ctr_dev_.get() + size_t(slot) * 2 * batch_cap_;
+            ps.step_meas = ps.step_spikes + batch_cap_;
             batch_slot& fl = slots_[slot];
             fl.t0 = t_;
             fl.b = b;
@@ -1267,8 +1270,7 @@ private:
             } else {
                 ps.log = nullptr;
             }
-            SYNQ_CUDA(cudaMemsetAsync(ps.step_spikes, 0, sizeof(uint32_t) * b, stream_));
-            SYNQ_CUDA(cudaMemsetAsync(ps.step_meas, 0, sizeof(uint32_t) * b, stream_));
+            SYNQ_CUDA(cudaMemsetAsync(ps.step_spikes, 0, sizeof(uint32_t) * (batch_cap_ + b), stream_));
             if (!fl.ev[0])
                 for (auto& e : fl.ev) SYNQ_CUDA(cudaEventCreate(&e));
             SYNQ_CUDA(cudaEventRecord(fl.ev[0], stream_));
@@ -1282,9 +1284,9 @@ private:
             launches_ += 1;
             SYNQ_CUDA(cudaEventRecord(fl.ev[1], stream_));
             uint32_t* hb = step_buf_.data() + size_t(slot) * 2 * batch_cap_;
-            SYNQ_CUDA(cudaMemcpyAsync(hb, ps.step_spikes, sizeof(uint32_t) * b, cudaMemcpyDeviceToHost, stream_));
-            SYNQ_CUDA(cudaMemcpyAsync(hb + b, ps.step_meas, sizeof(uint32_t) * b, cudaMemcpyDeviceToHost, stream_));
-            d2h_bytes_ += 8ull * b;
+            SYNQ_CUDA(cudaMemcpyAsync(hb, ps.step_spikes, sizeof(uint32_t) * (batch_cap_ + b), cudaMemcpyDeviceToHost,
+                                      stream_));
+            d2h_bytes_ += 4ull * (batch_cap_ + b);
             SYNQ_CUDA(cudaEventRecord(fl.ev[2], stream_));
             t_ += b;
         }
@@ -1302,7 +1304,7 @@ private:
         // per-step bookkeeping, frames_consumed (engine.hpp:371-380)
         for (uint32_t k = 0; k < b; ++k) {
             step_spikes_host_.push_back(hb[k]);
-            step_measured_.push_back(hb[b + k]);
+            step_measured_.push_back(hb[batch_cap_ + k]);
             if (fl.t0 + k - int64_t(delay_) + 1 >= 0) ++counters_.frames_consumed;
         }
         counters_.steps += b;
@@ -1429,6 +1431,7 @@ private:
     uint32_t ntiles_update_ = 1;
     dev_array<int64_t> t_dev_, t0_dev_;
     dev_array<uint32_t> step_spikes_dev_, step_meas_dev_;
+    dev_array<uint32_t> step_ctr_dev_;  // persistent engine: 2 slots x {spikes, measured} x batch_cap
     pinned_array<uint32_t> step_buf_;
     dev_array<uint32_t> det_cnt_, det_off_, det_fill_;
     dev_array<unsigned long long> det_ev_;
