@@ -22,6 +22,7 @@
 //   glibc and patched in.  The table is therefore bit-identical to the
 //   reference's.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -29,6 +30,7 @@
 #include <fstream>
 #include <numeric>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include "synq/adjacency.hpp"
@@ -311,16 +313,28 @@ device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons
     const char* prof_env = std::getenv("SYNQ_PLAN_PROFILE");
     if (prof_env && std::atoi(prof_env) != 0)
         std::fprintf(stderr, "expand: %zu jobs recomputed on the host\n", fl.size());
-    std::vector<uint32_t> buf;
-    for (uint64_t j : fl) {
-        const dev_job& job = jobs[j];
-        buf.resize(job.n);
-        xorshift r(derive_seed(seed, job.index + 1));
-        sorted_random(job.n, job.a, job.b, r, buf.data());
-        SYNQ_CUDA(cudaMemcpyAsync(g.cells.get() + job.o, buf.data(), job.n * sizeof(uint32_t),
+    // independent jobs: recompute them on all host cores, then upload
+    std::vector<std::vector<uint32_t>> outs(fl.size());
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+        for (size_t i; (i = next.fetch_add(1)) < fl.size();) {
+            const dev_job& job = jobs[fl[i]];
+            outs[i].resize(job.n);
+            xorshift r(derive_seed(seed, job.index + 1));
+            sorted_random(job.n, job.a, job.b, r, outs[i].data());
+        }
+    };
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16));
+    std::vector<std::thread> pool;
+    for (unsigned k = 1; k < nt && k < fl.size(); ++k) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    for (size_t i = 0; i < fl.size(); ++i) {
+        const dev_job& job = jobs[fl[i]];
+        SYNQ_CUDA(cudaMemcpyAsync(g.cells.get() + job.o, outs[i].data(), job.n * sizeof(uint32_t),
                                   cudaMemcpyHostToDevice, stream));
-        SYNQ_CUDA(cudaStreamSynchronize(stream));
     }
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
     g.tie_fixups = fl.size();
     return g;
 }
