@@ -36,7 +36,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -68,6 +67,37 @@ def parse():
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def ensure_world(args) -> None:
+    """--gpus N is the world size.  Without torchrun env vars and N > 1 this
+    process re-launches itself under torch.distributed.run (one rank per
+    GPU, rendezvous on 127.0.0.1); under torchrun WORLD_SIZE must equal N."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    if args.impl == "synq" and not (args.backend == "gloo"):
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have} "
+                             "(one rank per GPU; NCCL refuses two ranks on one device)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 # ------------------------------------------------------------ clocks
@@ -262,6 +292,7 @@ def run_reference_arm(args):
 # ------------------------------------------------------------ B200 arm
 def main():
     args = parse()
+    ensure_world(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     rank, world, local = dist_env()
@@ -280,18 +311,6 @@ def main():
     # the CUDA runtime picks the device from the current context: bind it
     if world > 1:
         torch.cuda.synchronize()
-
-    cpu_result = {}
-    cpu_thread = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        def _cpu():
-            try:
-                cpu_result.update(cpu_reference_sample(args.synapses, args.seed,
-                                                       args.cpu_sample_steps, 1, True))
-            except Exception as e:  # reported, never fatal
-                cpu_result["error"] = str(e)
-        cpu_thread = threading.Thread(target=_cpu, daemon=True)
-        cpu_thread.start()
 
     t_setup = time.perf_counter()
     opts = synq.Opts(seed=args.seed + rank, deterministic=True)
@@ -426,11 +445,20 @@ def main():
                    "log into pinned host memory, batches pipelined) + synq_sim_raster_copy into host "
                    "numpy buffers per step, wall clock, after one untimed recorded second",
             "raster_bytes_last_step": raster_bytes_host,
+            "inputs": "no per-step host inputs: the network is built on the device from the seed "
+                      "(h2d counts only control words); the per-step output is the spike raster",
         },
         "clocks": clocks.summary(),
     }
-    if cpu_thread is not None:
-        cpu_thread.join()
+    # the CPU reference sample runs after every GPU timed region (it builds a
+    # 4.2 GB network and would share host memory bandwidth with the e2e leg)
+    sim.close()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_result = {}
+        try:
+            cpu_result.update(cpu_reference_sample(args.synapses, args.seed, args.cpu_sample_steps, 1, True))
+        except Exception as e:  # reported, never fatal
+            cpu_result["error"] = str(e)
         if "error" in cpu_result:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": "failed: " + cpu_result["error"]}
@@ -444,7 +472,6 @@ def main():
                 "wall_s_per_bio_s": cpu_result["sim_s"] * BIO_STEPS / cpu_result["steps"],
             }
     print(json.dumps(line))
-    sim.close()
     return 0
 
 

@@ -81,6 +81,8 @@ struct persist_state {
     // receives with due >= log_from, in piece (= ascending id) order
     uint32_t* log;
     unsigned long long* log_end;  // out: entries written
+    uint32_t* log_cnt;            // out: ids logged per frame, index f - log_from (the
+                                  // merged frame of every publisher, remote ranks included)
     unsigned long long log_cap;
     int64_t log_from;
     uint32_t* flags;
@@ -488,6 +490,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         }
         const uint32_t S = seg_cur[P];
         const bool logging = ps.log && c == 0 && due >= ps.log_from;
+        if (logging && tid == 0) ps.log_cnt[due - ps.log_from] = S;
         for (uint32_t c0 = 0; c0 < S; c0 += NT) {
             // one spike per thread: id, this CTA's row segment, item count
             const uint32_t g = c0 + tid;
@@ -612,6 +615,7 @@ __global__ void k_log_drain(persist_state<M> ps, int64_t from, int64_t to) {
         }
         __syncthreads();
         const uint32_t S = s_seg[P];
+        if (threadIdx.x == 0) ps.log_cnt[f - from] = S;
         for (uint32_t j = 0; j < P; ++j) {
             const uint32_t cnt = s_seg[j + 1] - s_seg[j];
             for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x)

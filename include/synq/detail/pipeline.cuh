@@ -604,7 +604,10 @@ __global__ void __launch_bounds__(NT, 1)
                             s_ft_lb[sl] = logged ? lc : ~0ull;
                             s_ft_done[sl] = 0;
                         }
-                        if (logged) lc += S;
+                        if (logged) {
+                            if (lane == 0) ps.log_cnt[fbase + r_poll - ps.log_from] = S;
+                            lc += S;
+                        }
                         wend += nb;
                         __syncwarp();
                         if (lane == 0) st_release_cta(&s_work_end, wend);
@@ -755,6 +758,8 @@ __global__ void __launch_bounds__(NT, 1)
             for (int q = 1; q <= MB; ++q)
                 if (static_cast<uint32_t>(q) == wlog) flog = fpre[q];
             const unsigned long long lbase = lc - flog;
+            if (log_cta && dtid == 0)
+                for (uint32_t w = wlog; w < B; ++w) ps.log_cnt[fbase + r_next + w - ps.log_from] = s_seg[w][P];
             if constexpr (BM) {
                 // ---- bitmap delivery: per spike, this CTA's receive window is
                 // WQ x 128 bits of the spike's bitmap row.  Stage the windows of

@@ -474,9 +474,12 @@ public:
         return out;
     }
 
+    // On a shard the tap sees the merged frame of every rank.  With the
+    // in-engine exchange every frame is emitted before run() returns; on a
+    // manually exchanged shard a frame is emitted once it is delivered, i.e.
+    // in the run() after the other ranks' frames of it were imported (so the
+    // last delay-1 frames trail now()).
     void set_spike_tap(tap_fn fn) {
-        if (fn && sharded() && !opt_.shard_nccl)
-            throw std::invalid_argument("spike taps need the in-engine exchange on a shard");
         tap_ = std::move(fn);
         if (tap_) {
             ensure_log();
@@ -542,7 +545,8 @@ public:
         m.neuron_fields = detail::field_bytes<neuron_fields>() * n_;
         m.neuron_rng = uses_rng ? uint64_t(n_) * sizeof(xorshift) : 0;
         m.spike_bitmasks = hist_.bytes();
-        m.spike_queues = queue_.bytes() + qcount_.bytes() + finfo_.bytes() + xsend_.bytes() + xrecv_.bytes();
+        m.spike_queues = queue_.bytes() + qcount_.bytes() + finfo_.bytes() + xsend_.bytes() + xrecv_.bytes() +
+                         step_ctr_dev_.bytes() + step_spikes_dev_.bytes() + step_meas_dev_.bytes();
         m.ages = has_synapses ? uint64_t(n_) * 4 : 0;
         m.expirations = has_synapses ? uint64_t(n_) * 4 : 0;
         m.adjacency = graph_.bytes() + split_.bytes() + bm_.bytes();  // + receive-window bitmaps
@@ -892,6 +896,11 @@ private:
         const uint64_t frames = cap / std::max<uint32_t>(1, n_);
         const uint64_t fit = frames > delay_ ? frames - delay_ : 1;
         batch_cap_ = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(batch_cap_, fit)));
+        if (persistent_) {
+            // logged ids per frame (a batch logs <= batch_cap_ frames, the drain <= delay)
+            plog_cnt_[0].resize(size_t(batch_cap_) + delay_ + 1);
+            plog_cnt_[1].resize(size_t(batch_cap_) + delay_ + 1);
+        }
     }
 
     dev::engine_state<Model> state() {
@@ -1251,10 +1260,10 @@ private:
     void launch_persistent(uint32_t b, int slot) {
         if constexpr (population_model) {
             auto ps = pstate();
-            // one counter block per slot: spikes [0, cap), measured [cap, cap + b),
-            // so a batch costs one memset and one copy
+            // one counter block per slot: spikes [0, b), measured [b, 2b), so a
+            // batch costs one memset and one copy of 2b words
             ps.step_spikes = step_ctr_dev_.get() + size_t(slot) * 2 * batch_cap_;
-            ps.step_meas = ps.step_spikes + batch_cap_;
+            ps.step_meas = ps.step_spikes + b;
             batch_slot& fl = slots_[slot];
             fl.t0 = t_;
             fl.b = b;
@@ -1262,15 +1271,17 @@ private:
             if (log_on_) {
                 ps.log = plog_[slot].get();
                 ps.log_end = plog_end_.get() + slot;
+                ps.log_cnt = plog_cnt_[slot].get();
                 ps.log_cap = log_cap_;
                 ps.log_from = log_pred_;
+                fl.log_from = log_pred_;
                 plog_end_[slot] = 0;
                 // frames logged_upto_ .. t_end-delay are emitted when it finishes
                 log_pred_ = std::max(log_pred_, t_ + int64_t(b) - int64_t(delay_) + 1);
             } else {
                 ps.log = nullptr;
             }
-            SYNQ_CUDA(cudaMemsetAsync(ps.step_spikes, 0, sizeof(uint32_t) * (batch_cap_ + b), stream_));
+            SYNQ_CUDA(cudaMemsetAsync(ps.step_spikes, 0, sizeof(uint32_t) * 2 * b, stream_));
             if (!fl.ev[0])
                 for (auto& e : fl.ev) SYNQ_CUDA(cudaEventCreate(&e));
             SYNQ_CUDA(cudaEventRecord(fl.ev[0], stream_));
@@ -1284,9 +1295,8 @@ private:
             launches_ += 1;
             SYNQ_CUDA(cudaEventRecord(fl.ev[1], stream_));
             uint32_t* hb = step_buf_.data() + size_t(slot) * 2 * batch_cap_;
-            SYNQ_CUDA(cudaMemcpyAsync(hb, ps.step_spikes, sizeof(uint32_t) * (batch_cap_ + b), cudaMemcpyDeviceToHost,
-                                      stream_));
-            d2h_bytes_ += 4ull * (batch_cap_ + b);
+            SYNQ_CUDA(cudaMemcpyAsync(hb, ps.step_spikes, sizeof(uint32_t) * 2 * b, cudaMemcpyDeviceToHost, stream_));
+            d2h_bytes_ += 8ull * b;
             SYNQ_CUDA(cudaEventRecord(fl.ev[2], stream_));
             t_ += b;
         }
@@ -1304,7 +1314,7 @@ private:
         // per-step bookkeeping, frames_consumed (engine.hpp:371-380)
         for (uint32_t k = 0; k < b; ++k) {
             step_spikes_host_.push_back(hb[k]);
-            step_measured_.push_back(hb[batch_cap_ + k]);
+            step_measured_.push_back(hb[b + k]);
             if (fl.t0 + k - int64_t(delay_) + 1 >= 0) ++counters_.frames_consumed;
         }
         counters_.steps += b;
@@ -1312,7 +1322,8 @@ private:
             const uint64_t end = plog_end_[slot];
             if (end > log_cap_) throw device_error("spike log overflow (batch too large for the frame log)");
             d2h_bytes_ += 8 + 4 * end;  // written to host memory by the kernel
-            emit_logged(plog_[slot].data(), end, fl.t0 + int64_t(b) - int64_t(delay_));
+            emit_logged(plog_[slot].data(), end, fl.t0 + int64_t(b) - int64_t(delay_), plog_cnt_[slot].data(),
+                        fl.log_from);
         }
     }
 
@@ -1320,11 +1331,15 @@ private:
         return 2 + (has_synapses ? 1 : 0) + (exact_ ? 3 : 0);
     }
 
-    // frames logged_upto_ .. last are the next entries of `log`, in order
-    void emit_logged(const uint32_t* log, uint64_t logged, int64_t last) {
+    // frames logged_upto_ .. last are the next entries of `log`, in order.
+    // cnts[f - cnt_from]: ids logged for frame f by the persistent kernel (the
+    // merged frame; on a shard step_spikes_host_ only counts local spikes),
+    // else the per-step spike counts of the generic engine
+    void emit_logged(const uint32_t* log, uint64_t logged, int64_t last, const uint32_t* cnts = nullptr,
+                     int64_t cnt_from = 0) {
         uint64_t off = 0;
         for (int64_t f = logged_upto_; f <= last; ++f) {
-            const uint32_t cnt = step_spikes_host_[static_cast<size_t>(f)];
+            const uint32_t cnt = cnts ? cnts[f - cnt_from] : step_spikes_host_[static_cast<size_t>(f)];
             const uint64_t a = std::min(off, logged), e = std::min(off + cnt, logged);
             off += cnt;
             emit(f, std::span<const uint32_t>(log + a, e - a));
@@ -1338,6 +1353,7 @@ private:
             auto ps = pstate();
             ps.log = plog_[0].get();
             ps.log_end = plog_end_.get();
+            ps.log_cnt = plog_cnt_[0].get();
             ps.log_cap = log_cap_;
             plog_end_[0] = 0;
             dev::k_log_drain<Model><<<1, 1024, 0, stream_>>>(ps, logged_upto_, t_ - 1);
@@ -1346,7 +1362,7 @@ private:
             SYNQ_CUDA(cudaStreamSynchronize(stream_));
             const uint64_t logged = std::min<uint64_t>(plog_end_[0], log_cap_);
             d2h_bytes_ += 8 + 4 * logged;
-            emit_logged(plog_[0].data(), logged, t_ - 1);
+            emit_logged(plog_[0].data(), logged, t_ - 1, plog_cnt_[0].data(), logged_upto_);
         }
     }
 
@@ -1444,8 +1460,10 @@ private:
     bool log_on_ = false;
     pinned_array<uint32_t> plog_[2];          // persistent engine: frame logs, one per batch slot
     pinned_array<unsigned long long> plog_end_;
+    pinned_array<uint32_t> plog_cnt_[2];  // ids logged per frame, one per batch slot
     struct batch_slot {
         int64_t t0 = 0;
+        int64_t log_from = 0;
         uint32_t b = 0;
         bool logging = false;
         cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // kernel start, kernel end, copies done

@@ -19,6 +19,11 @@
 //        OUT.state (f32 fields), OUT.syn (brunel+ synapse fields after flush),
 //        OUT.counters (text)
 //   synq_golden run_desc MODEL DESC SEED STEPS OUT
+//   synq_golden big MODEL SYNAPSES SEED STEPS OUT
+//        network sized like synq_sim_new_for_synapses (solve_neurons,
+//        benchmarks.cpp:220-249), deterministic run; OUT.adj
+//        (adjacency_list::save_file of the built graph), OUT.frames,
+//        OUT.state, OUT.counters as for `run`
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -132,6 +137,16 @@ void dump_run(network<M>& net, int64_t steps, const std::string& out) {
 }
 
 template <class M>
+void big_run(model_build<M> b, uint64_t seed, int64_t steps, const std::string& out) {
+    engine_options opt;
+    opt.seed = seed;
+    opt.deterministic = true;
+    network<M> net(b.desc, b.model, opt);
+    net.graph().save_file(out + ".adj");
+    dump_run(net, steps, out);
+}
+
+template <class M>
 void run_model(model_build<M> b, uint64_t seed, int64_t steps, const std::string& out,
                uint32_t history) {
     engine_options opt;
@@ -231,6 +246,20 @@ int main(int argc, char** argv) {
             return run_cmd(argv[2], nullptr, std::strtoul(argv[3], nullptr, 0),
                            std::strtoull(argv[4], nullptr, 0), std::strtoll(argv[5], nullptr, 0),
                            argv[6], hist, dt, delay);
+        } else if (cmd == "big") {
+            const std::string model = argv[2];
+            param_set ps = builtin_defaults();
+            const uint32_t n = solve_neurons(parse_model(model), std::strtoull(argv[3], nullptr, 0), ps);
+            const uint64_t seed = std::strtoull(argv[4], nullptr, 0);
+            const int64_t steps = std::strtoll(argv[5], nullptr, 0);
+            if (model == "brunel")
+                big_run(build_brunel(n, ps), seed, steps, argv[6]);
+            else if (model == "brunel+")
+                big_run(build_brunel_plus(n, ps), seed, steps, argv[6]);
+            else if (model == "vogels")
+                big_run(build_vogels(n, ps), seed, steps, argv[6]);
+            else
+                return 2;
         } else if (cmd == "run_desc") {
             network_desc d = load_desc(argv[3]);
             return run_cmd(argv[2], &d, 0, std::strtoull(argv[4], nullptr, 0),

@@ -27,9 +27,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <fstream>
 #include <numeric>
 #include <stdexcept>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -313,28 +315,54 @@ device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons
     const char* prof_env = std::getenv("SYNQ_PLAN_PROFILE");
     if (prof_env && std::atoi(prof_env) != 0)
         std::fprintf(stderr, "expand: %zu jobs recomputed on the host\n", fl.size());
-    // independent jobs: recompute them on all host cores, then upload
-    std::vector<std::vector<uint32_t>> outs(fl.size());
-    std::atomic<size_t> next{0};
-    auto work = [&] {
-        for (size_t i; (i = next.fetch_add(1)) < fl.size();) {
-            const dev_job& job = jobs[fl[i]];
-            outs[i].resize(job.n);
-            xorshift r(derive_seed(seed, job.index + 1));
-            sorted_random(job.n, job.a, job.b, r, outs[i].data());
-        }
-    };
+    // independent jobs: recompute them on all host cores, then upload.  In
+    // chunks of at most kChunkWords output words (one staging buffer, one sync
+    // per chunk), so even the recompute-everything fallback stays bounded; a
+    // worker's exception (bad_alloc ...) is rethrown here, after the join, so
+    // guarded() maps it to a status instead of std::terminate
+    constexpr uint64_t kChunkWords = uint64_t(1) << 24;  // 64 MB
     const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16));
-    std::vector<std::thread> pool;
-    for (unsigned k = 1; k < nt && k < fl.size(); ++k) pool.emplace_back(work);
-    work();
-    for (auto& th : pool) th.join();
-    for (size_t i = 0; i < fl.size(); ++i) {
-        const dev_job& job = jobs[fl[i]];
-        SYNQ_CUDA(cudaMemcpyAsync(g.cells.get() + job.o, outs[i].data(), job.n * sizeof(uint32_t),
-                                  cudaMemcpyHostToDevice, stream));
+    std::vector<uint32_t> stage;
+    std::vector<uint64_t> at;  // staging offset of each job of the chunk
+    for (size_t q0 = 0; q0 < fl.size();) {
+        size_t q1 = q0;
+        uint64_t words = 0;
+        at.clear();
+        while (q1 < fl.size() && (q1 == q0 || words + jobs[fl[q1]].n <= kChunkWords)) {
+            at.push_back(words);
+            words += jobs[fl[q1]].n;
+            ++q1;
+        }
+        stage.resize(std::max<uint64_t>(1, words));
+        std::atomic<size_t> next{q0};
+        std::exception_ptr err;
+        std::mutex err_mu;
+        auto work = [&] {
+            try {
+                for (size_t i; (i = next.fetch_add(1)) < q1;) {
+                    const dev_job& job = jobs[fl[i]];
+                    xorshift r(derive_seed(seed, job.index + 1));
+                    sorted_random(job.n, job.a, job.b, r, stage.data() + at[i - q0]);
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(err_mu);
+                if (!err) err = std::current_exception();
+                next.store(q1);
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned k = 1; k < nt && k < q1 - q0; ++k) pool.emplace_back(work);
+        work();
+        for (auto& th : pool) th.join();
+        if (err) std::rethrow_exception(err);
+        for (size_t i = q0; i < q1; ++i) {
+            const dev_job& job = jobs[fl[i]];
+            SYNQ_CUDA(cudaMemcpyAsync(g.cells.get() + job.o, stage.data() + at[i - q0], job.n * sizeof(uint32_t),
+                                      cudaMemcpyHostToDevice, stream));
+        }
+        SYNQ_CUDA(cudaStreamSynchronize(stream));  // the staging buffer is reused by the next chunk
+        q0 = q1;
     }
-    SYNQ_CUDA(cudaStreamSynchronize(stream));
     g.tie_fixups = fl.size();
     return g;
 }

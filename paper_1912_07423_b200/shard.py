@@ -145,9 +145,12 @@ class ShardGroup:
     """
 
     def __init__(self, model: str, neurons: int, world: int, record: bool = False, exchange: str = "words",
-                 **opts):
+                 engine_record: bool = False, **opts):
+        # record: merge the exported frames here; engine_record: every shard
+        # also records the merged frames through its own engine log
         self.world = world
-        self.sims = [Sim(model, neurons, Opts(shard=(r, world), **opts)) for r in range(world)]
+        self.sims = [Sim(model, neurons, Opts(shard=(r, world), record=engine_record or None, **opts))
+                     for r in range(world)]
         self.delay = self.sims[0].delay
         self.record = record
         self.exchange = exchange  # "words" (host wire format) or "bits" (the in-engine bitmask blocks)

@@ -28,4 +28,5 @@ def golden():
         "plans": np.load(os.path.join(d, "plans.npz")),
         "adj": np.load(os.path.join(d, "adjacency.npz")),
         "runs": np.load(os.path.join(d, "runs.npz")),
+        "big": np.load(os.path.join(d, "big.npz")),
     }

@@ -128,12 +128,91 @@ def run_vectors():
     return meta
 
 
+# the benchmarked configuration (BASELINE.json configs[1]): Brunel sized for
+# ~1e9 synapses through solve_neurons (synq_sim_new_for_synapses), seed 1,
+# one full biological second (10,000 steps; past the step-2,213 point where
+# the reference's own parallel and deterministic modes part)
+BIG = [("brunel", 1_000_000_000, 1, 10_000)]
+
+
+def frame_digests(counts: np.ndarray, ids: np.ndarray) -> np.ndarray:
+    """u64 per step: the first 8 bytes (little endian) of sha256 of the
+    frame's ids as u32 LE (tests/test_gpu_parity_big.py recomputes it)."""
+    out = np.empty(len(counts), np.uint64)
+    off = 0
+    for k, c in enumerate(counts):
+        h = hashlib.sha256(np.ascontiguousarray(ids[off:off + c], "<u4").tobytes()).digest()
+        out[k] = int.from_bytes(h[:8], "little")
+        off += c
+    return out
+
+
+def big_vectors(workdir: str = "/tmp/synq_big"):
+    """Reference run at the bench configuration, reduced to fixtures: the
+    adjacency (sha256 of the whole table, per-1024-row block digests, the
+    degree vector), per-step frame counts and digests, final V / ACC / REF
+    (sha256 + the first 4096 values) and the counters."""
+    os.makedirs(workdir, exist_ok=True)
+    out, meta = {}, {}
+    for model, syn, seed, steps in BIG:
+        tag = f"{model.replace('+', 'p')}_{syn:.0e}_s{seed}_t{steps}".replace("+", "")
+        base = os.path.join(workdir, tag)
+        if not os.path.exists(base + ".counters"):
+            O.golden("big", model, syn, seed, steps, base)
+        raw = np.memmap(base + ".adj", np.uint32, "r")
+        neurons, pitch, deg_max, sentinel = (int(x) for x in raw[:4])
+        cells = raw[4:4 + neurons * pitch].reshape(neurons, pitch)
+        h = hashlib.sha256()
+        blocks = []
+        deg = np.empty(neurons, np.uint32)
+        for r0 in range(0, neurons, 1024):
+            blk = np.ascontiguousarray(cells[r0:r0 + 1024])
+            b = blk.tobytes()
+            h.update(b)
+            blocks.append(int.from_bytes(hashlib.sha256(b).digest()[:8], "little"))
+            deg[r0:r0 + len(blk)] = (blk != sentinel).sum(1)
+        fr = np.fromfile(base + ".frames", np.uint32)
+        counts, parts, off = [], [], 0
+        while off < len(fr):
+            c = int(fr[off])
+            counts.append(c)
+            parts.append(fr[off + 1: off + 1 + c])
+            off += 1 + c
+        counts = np.array(counts, np.uint32)
+        ids = np.concatenate(parts) if parts else np.zeros(0, np.uint32)
+        st = np.fromfile(base + ".state", np.uint32).reshape(3, neurons)
+        counters = {}
+        for line in open(base + ".counters"):
+            k, v = line.strip().split("=")
+            counters[k] = int(v)
+        out[f"{tag}_deg"] = deg
+        out[f"{tag}_blocks"] = np.array(blocks, np.uint64)
+        out[f"{tag}_counts"] = counts
+        out[f"{tag}_digests"] = frame_digests(counts, ids)
+        for i in range(3):
+            out[f"{tag}_f{i}_head"] = st[i, :4096].copy()
+        meta[tag] = {"model": model, "synapses": syn, "seed": seed, "steps": steps, "neurons": neurons,
+                     "pitch": pitch, "deg_max": deg_max, "edges": int(deg.sum()), "adj_sha256": h.hexdigest(),
+                     "state_sha256": [hashlib.sha256(st[i].tobytes()).hexdigest() for i in range(3)],
+                     "counters": counters}
+    np.savez_compressed(os.path.join(HERE, "big.npz"), **out)
+    return meta
+
+
 def main():
     if not O.have_reference():
         raise SystemExit("oracle/_ref not built (needs /root/reference): make -C oracle")
+    if sys.argv[1:] == ["big"]:
+        path = os.path.join(HERE, "golden.json")
+        meta = json.load(open(path))
+        meta["big"] = big_vectors()
+        with open(path, "w") as fh:
+            json.dump(meta, fh, indent=1, sort_keys=True)
+        print("big fixtures written to", HERE)
+        return
     rng_vectors()
     plan_vectors()
-    meta = {"adjacency": adj_vectors(), "runs": run_vectors()}
+    meta = {"adjacency": adj_vectors(), "runs": run_vectors(), "big": big_vectors()}
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
     print("golden fixtures written to", HERE)

@@ -49,6 +49,8 @@ def test_help_and_version(cli):
     (["--model", "brunel", "--sweep", "1e6,0.5"], 1, "sweep sizes must be >= 1"),
     (["--model", "brunel", "--neurons", "10", "--param", "noequals"], 1, "bad --param"),
     (["--model", "brunel", "--neurons", "10", "--param", "j=abc"], 1, "bad --param value"),
+    (["--model", "brunel", "--neurons", "10", "--delay", "4294967297"], 1, "--delay must fit 32 bits"),
+    (["--model", "brunel", "--neurons", "10", "--threads", "4294967296"], 1, "--threads must fit 32 bits"),
 ])
 def test_usage_errors(cli, args, code, msg):
     r = run(cli, *args)

@@ -172,3 +172,24 @@ def test_nccl_in_engine_single_rank(golden):
             assert np.array_equal(sim.neuron_field(i).view(np.uint32), runs[f"{tag}_f{i}"]), (tag, i)
         assert sim.counters()["deliveries"] == m["counters"]["deliveries"], tag
         sim.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_engine_log_segments_merged_frames(golden, world):
+    """Every shard records through its own engine log (CTA 0 logs the merged
+    frame, remote ranks' pieces included).  The log must be cut into steps by
+    the merged per-frame counts, not by the shard's local spike counts: each
+    shard's raster equals the reference frames up to the last delivered one."""
+    runs = golden["runs"]
+    for tag, m in population_runs(golden):
+        g = group(m, world, "bits", engine_record=True)
+        g.run(m["steps"])
+        done = m["steps"] - g.delay + 1  # frames delivered (the rest await the next exchange)
+        want_c = runs[f"{tag}_counts"][:done]
+        want_ids = runs[f"{tag}_ids"][: int(want_c.sum())]
+        for s in g.sims:
+            counts, ids = s.frames()
+            assert np.array_equal(counts[:done], want_c), (tag, world)
+            assert np.array_equal(ids[: int(want_c.sum())], want_ids), (tag, world)
+            assert counts[done:].sum() == 0
+        g.close()

@@ -208,3 +208,15 @@ def test_lif_decay_kat():
     v = np.float32(10.0)
     v = np.float32(v + (np.float32(1.0) * (-(v - np.float32(0.0)) / np.float32(20.0)) + np.float32(0)))
     assert abs(float(v) - 9.5) < 1e-6
+
+
+def test_big_fixture_is_self_consistent(golden):
+    """tests/golden/big.npz (Brunel 1e9 from the reference) agrees with its
+    own metadata: degrees sum to the edges, counts to the spikes."""
+    for tag, m in golden["meta"]["big"].items():
+        big = golden["big"]
+        assert int(big[f"{tag}_deg"].astype(np.uint64).sum()) == m["edges"] == m["counters"]["edges"]
+        assert int(big[f"{tag}_counts"].astype(np.uint64).sum()) == m["counters"]["spikes"]
+        assert len(big[f"{tag}_digests"]) == m["steps"]
+        assert int(big[f"{tag}_deg"].max()) == m["deg_max"]
+        assert m["pitch"] % 32 == 0 and m["pitch"] >= m["deg_max"]

@@ -184,6 +184,8 @@ int main(int argc, char** argv) {
         fail("model '" + a.model + "' needs --neurons, --synapses or --net");
     if (!(a.duration_s > 0)) fail("--duration must be > 0");
     if (a.neurons > 0xffffffffull) fail("--neurons must fit 32 bits");
+    if (a.delay > 0xffffffffull) fail("--delay must fit 32 bits");
+    if (a.threads > 0xffffffffull) fail("--threads must fit 32 bits");
 
     std::unique_ptr<synq_opts, opts_deleter> opts(synq_opts_new());
     if (!opts) fail("out of memory");
