@@ -19,11 +19,19 @@
 //        OUT.state (f32 fields), OUT.syn (brunel+ synapse fields after flush),
 //        OUT.counters (text)
 //   synq_golden run_desc MODEL DESC SEED STEPS OUT
+//   synq_golden sweep S P RATE SEED STEPS OUT
+//        the synthetic sweep model (include/synq/models/sweep.hpp, compiled
+//        here against the reference headers), N = round(sqrt(S/p)), one
+//        population self-connected with probability p, dt 0.1 ms, delay 15;
+//        deterministic run dumped like `run` (OUT.state = ACC)
+//   synq_golden sweep_time S P RATE SEED WARM STEPS THREADS DET
+//        CPU baseline of one sweep point: prints events / sim_s / construct_s
 //   synq_golden big MODEL SYNAPSES SEED STEPS OUT
 //        network sized like synq_sim_new_for_synapses (solve_neurons,
 //        benchmarks.cpp:220-249), deterministic run; OUT.adj
 //        (adjacency_list::save_file of the built graph), OUT.frames,
 //        OUT.state, OUT.counters as for `run`
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -39,6 +47,9 @@
 #include "synq/network_desc.hpp"
 #include "synq/params.hpp"
 #include "synq/random.hpp"
+// the sweep model is user code against the model concept: this repo's header,
+// resolved against the reference's own synq/soa.hpp (include path order)
+#include "../include/synq/models/sweep.hpp"
 
 using namespace synq;
 
@@ -146,6 +157,17 @@ void big_run(model_build<M> b, uint64_t seed, int64_t steps, const std::string& 
     dump_run(net, steps, out);
 }
 
+model_build<sweep_model> sweep_build(double S, double p, double rate) {
+    const uint32_t n = static_cast<uint32_t>(std::llround(std::sqrt(S / p)));
+    model_build<sweep_model> b;
+    b.desc.populations = {population_spec{n}};
+    b.desc.connections = {connectivity_spec{0, 0, p}};
+    b.desc.dt = 0.1;
+    b.desc.delay = 15;
+    b.model.p_spike = static_cast<float>(rate * 0.1 * 1e-3);
+    return b;
+}
+
 template <class M>
 void run_model(model_build<M> b, uint64_t seed, int64_t steps, const std::string& out,
                uint32_t history) {
@@ -246,6 +268,24 @@ int main(int argc, char** argv) {
             return run_cmd(argv[2], nullptr, std::strtoul(argv[3], nullptr, 0),
                            std::strtoull(argv[4], nullptr, 0), std::strtoll(argv[5], nullptr, 0),
                            argv[6], hist, dt, delay);
+        } else if (cmd == "sweep") {
+            auto b = sweep_build(std::atof(argv[2]), std::atof(argv[3]), std::atof(argv[4]));
+            run_model(b, std::strtoull(argv[5], nullptr, 0), std::strtoll(argv[6], nullptr, 0), argv[7], 0);
+        } else if (cmd == "sweep_time") {
+            auto b = sweep_build(std::atof(argv[2]), std::atof(argv[3]), std::atof(argv[4]));
+            engine_options opt;
+            opt.seed = std::strtoull(argv[5], nullptr, 0);
+            opt.threads = static_cast<unsigned>(std::strtoul(argv[8], nullptr, 0));
+            opt.deterministic = std::atoi(argv[9]) != 0;
+            network<sweep_model> net(b.desc, b.model, opt);
+            net.run(std::strtoll(argv[6], nullptr, 0));
+            const double t0 = net.timings().simulate;
+            const uint64_t d0 = net.counters().deliveries;
+            net.run(std::strtoll(argv[7], nullptr, 0));
+            std::printf("events=%llu\nsim_s=%.9f\nconstruct_s=%.6f\nneurons=%u\nsynapses=%llu\n",
+                        static_cast<unsigned long long>(net.counters().deliveries - d0), net.timings().simulate - t0,
+                        net.timings().construct, net.neuron_count(),
+                        static_cast<unsigned long long>(net.edge_count()));
         } else if (cmd == "big") {
             const std::string model = argv[2];
             param_set ps = builtin_defaults();

@@ -199,20 +199,55 @@ def big_vectors(workdir: str = "/tmp/synq_big"):
     return meta
 
 
+# synthetic sweep (BASELINE.json configs[3]) at a reduced budget: every
+# (p, rate) point of the bench grid, S = 1e6 synapses, seed 1, 2000 steps
+SWEEP_S, SWEEP_STEPS = 1_000_000, 2000
+SWEEP = [(p, r) for p in (0.1, 0.01, 0.001) for r in (1.0, 10.0, 100.0)]
+
+
+def sweep_vectors():
+    """Reference runs of the sweep model (include/synq/models/sweep.hpp built
+    against the reference headers): per-step counts + digests, final ACC
+    (sha256), counters."""
+    import tempfile
+    out, meta = {}, {}
+    for p, rate in SWEEP:
+        tag = f"sweep_p{p:g}_r{rate:g}"
+        with tempfile.TemporaryDirectory() as td:
+            base = os.path.join(td, "run")
+            O.golden("sweep", SWEEP_S, p, rate, 1, SWEEP_STEPS, base)
+            counts, ids = O.split_frames(np.fromfile(base + ".frames", np.uint32))
+            acc = np.fromfile(base + ".state", np.uint32)
+            counters = {}
+            for line in open(base + ".counters"):
+                k, v = line.strip().split("=")
+                counters[k] = int(v)
+        out[f"{tag}_counts"] = counts
+        out[f"{tag}_digests"] = frame_digests(counts, ids)
+        meta[tag] = {"S": SWEEP_S, "p": p, "rate": rate, "seed": 1, "steps": SWEEP_STEPS,
+                     "acc_sha256": hashlib.sha256(acc.tobytes()).hexdigest(), "counters": counters}
+    np.savez_compressed(os.path.join(HERE, "sweep.npz"), **out)
+    return meta
+
+
 def main():
     if not O.have_reference():
         raise SystemExit("oracle/_ref not built (needs /root/reference): make -C oracle")
-    if sys.argv[1:] == ["big"]:
+    if sys.argv[1:] and sys.argv[1] in ("big", "sweep"):
         path = os.path.join(HERE, "golden.json")
         meta = json.load(open(path))
-        meta["big"] = big_vectors()
+        if sys.argv[1] == "big":
+            meta["big"] = big_vectors()
+        else:
+            meta["sweep"] = sweep_vectors()
         with open(path, "w") as fh:
             json.dump(meta, fh, indent=1, sort_keys=True)
         print("big fixtures written to", HERE)
         return
     rng_vectors()
     plan_vectors()
-    meta = {"adjacency": adj_vectors(), "runs": run_vectors(), "big": big_vectors()}
+    meta = {"adjacency": adj_vectors(), "runs": run_vectors(), "big": big_vectors(),
+            "sweep": sweep_vectors()}
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
     print("golden fixtures written to", HERE)
