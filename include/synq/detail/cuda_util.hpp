@@ -76,12 +76,13 @@ public:
     size_t bytes() const { return n_ * sizeof(T); }
     explicit operator bool() const { return p_ != nullptr; }
 
-private:
     void release() {
         if (p_) cudaFree(p_);
         p_ = nullptr;
         n_ = 0;
     }
+
+private:
     T* p_ = nullptr;
     size_t n_ = 0;
 };

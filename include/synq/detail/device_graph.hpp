@@ -23,6 +23,10 @@ struct device_graph {
     uint64_t edges = 0;
     uint64_t jobs = 0;
     uint64_t tie_fixups = 0;  // jobs recomputed on the host by the rounding guard
+    // targets held: [target_lo, target_hi) (a shard's sub-rows, SURVEY.md 8e;
+    // the whole id space otherwise).  deg_max / pitch / edges / degree are
+    // those of the sub-rows.
+    uint32_t target_lo = 0, target_hi = 0;
     dev_array<uint32_t> cells;
     dev_array<uint32_t> degree;
     std::vector<uint32_t> host_degree;
@@ -34,11 +38,14 @@ struct device_graph {
 // construction_plan as the host plan_jobs, bit for bit
 construction_plan plan_jobs_device(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
                                    cudaStream_t stream);
-// plan on the device (SYNQ_HOST_PLAN=1: on the host), expand on the device
+// plan on the device (SYNQ_HOST_PLAN=1: on the host), expand on the device.
+// [tlo, thi): keep only the targets in this range (every row's sub-row, still
+// sorted; pitch = that sub-row maximum rounded up to pitch_align): the
+// storage of one shard of a target-partitioned multi-GPU run.
 device_graph build_device_graph(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
-                                cudaStream_t stream);
+                                cudaStream_t stream, uint32_t tlo = 0, uint32_t thi = 0xffffffffu);
 device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons, uint64_t seed,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, uint32_t tlo, uint32_t thi, uint32_t pitch_align);
 // host mirror of a device graph
 adjacency_list download_graph(const device_graph& g, cudaStream_t stream);
 // upload a host table (adjacency_list::load) to the device

@@ -170,7 +170,16 @@ public:
         for (auto& e : ev_) SYNQ_CUDA(cudaEventCreate(&e));
 
         auto t0 = clock::now();
-        graph_ = build_device_graph(desc_, opt_.seed, opt_.pitch_align, stream_);
+        // a shard of a multi-GPU run stores only the sub-rows of the targets
+        // it receives for: ~1/W of the synapses per GPU
+        uint32_t tlo = 0, thi = 0xffffffffu;
+        if (opt_.shard_world > 1) {
+            if (opt_.shard_rank >= opt_.shard_world) throw std::invalid_argument("shard rank out of range");
+            cut_ = shard_cut_of(desc_, opt_.shard_world);
+            tlo = cut_.ra[opt_.shard_rank];
+            thi = cut_.ra[opt_.shard_rank + 1];
+        }
+        graph_ = build_device_graph(desc_, opt_.seed, opt_.pitch_align, stream_, tlo, thi);
         timings_.construct = since(t0);
 
         if constexpr (has_synapses) {
@@ -343,10 +352,21 @@ public:
     uint64_t synapse_capacity() const {
         return has_synapses ? static_cast<uint64_t>(n_) * graph_.deg_max : 0;
     }
+    // host mirror of the adjacency; a shard holds (and returns) the sub-rows
+    // of its own targets [graph_targets()), rebuilt if they were released
     const adjacency_list& graph() const {
-        if (!adj_mirror_) adj_mirror_ = std::make_unique<adjacency_list>(download_graph(graph_, stream_));
+        if (!adj_mirror_) {
+            if (graph_.cells || graph_.edges == 0) {
+                adj_mirror_ = std::make_unique<adjacency_list>(download_graph(graph_, stream_));
+            } else {
+                const device_graph g = build_device_graph(desc_, opt_.seed, opt_.pitch_align, stream_,
+                                                          graph_.target_lo, graph_.target_hi);
+                adj_mirror_ = std::make_unique<adjacency_list>(download_graph(g, stream_));
+            }
+        }
         return *adj_mirror_;
     }
+    std::pair<uint32_t, uint32_t> graph_targets() const { return {graph_.target_lo, graph_.target_hi}; }
     const network_desc& desc() const { return desc_; }
     const engine_counters& counters() const { return counters_; }
     const phase_seconds& timings() const { return timings_; }
@@ -603,6 +623,9 @@ private:
             throw std::invalid_argument("sharding needs a delay of at least 2 steps (frames are exchanged every delay-1 steps)");
         if constexpr (population_model)
             if (sharded()) setup_exchange();
+        // a shard delivering from window bitmaps never reads its ELL sub-rows
+        // again: release them (graph() rebuilds them on demand)
+        if (opt_.shard_world > 1 && persistent_ && pipe_ && pipe_bm_) graph_.cells.release();
         Q_ = persistent_ ? 2 * delay_ : delay_;
         queue_.resize(std::max<size_t>(1, size_t(Q_) * n_));
         qcount_.resize(Q_);
@@ -620,6 +643,81 @@ private:
         step_buf_.resize(4 * size_t(batch_cap_));
     }
 
+    // ---- partition helpers (setup_persistent; shard construction)
+    struct shard_cut {
+        uint32_t r0 = 0, r1 = 0, u0 = 0, u1 = 0;  // receiving / update-only regions
+        bool u_after = true;                      // update-only region after the receiving one
+        std::vector<uint32_t> ra, ub;             // W rank ranges of each (W + 1 bounds)
+    };
+    static double receive_cost(double indeg) { return 16.0 + 0.003 * indeg; }
+    // ids [lo, hi) of a region starting at r0 cut into `parts` ranges of equal
+    // prefix cost
+    static std::vector<uint32_t> cut_by_cost(const std::vector<double>& prefix, uint32_t r0, uint32_t lo,
+                                             uint32_t hi, uint32_t parts) {
+        std::vector<uint32_t> b(parts + 1);
+        const double c0 = prefix[lo - r0], c1 = prefix[hi - r0];
+        for (uint32_t c = 0; c <= parts; ++c) {
+            const double target = c0 + (c1 - c0) * c / parts;
+            b[c] = r0 + static_cast<uint32_t>(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
+            b[c] = std::clamp(b[c], lo, hi);
+        }
+        b[0] = lo;
+        b[parts] = hi;
+        for (uint32_t c = 1; c <= parts; ++c) b[c] = std::max(b[c], b[c - 1]);
+        return b;
+    }
+    static std::vector<uint32_t> cut_by_count(uint32_t lo, uint32_t hi, uint32_t parts) {
+        std::vector<uint32_t> b(parts + 1);
+        for (uint32_t c = 0; c <= parts; ++c) b[c] = lo + static_cast<uint32_t>(uint64_t(hi - lo) * c / parts);
+        return b;
+    }
+    // the receiving region [r0, r1) (neurons outside receive nothing) and the
+    // update-only remainder, which must be one range on one side, else the
+    // whole id space is the receiving region (B pieces stay empty)
+    template <class T>
+    static shard_cut region_of(const std::vector<T>& indeg, uint32_t n) {
+        shard_cut k;
+        uint32_t r0 = 0, r1 = 0;
+        while (r0 < n && indeg[r0] == 0) ++r0;
+        r1 = n;
+        while (r1 > r0 && indeg[r1 - 1] == 0) --r1;
+        if (r0 == r1) r0 = r1 = 0;
+        k.u0 = r1;
+        k.u1 = n;
+        if (r0 > 0 && r1 < n) {
+            r0 = 0;
+            r1 = n;
+            k.u0 = k.u1 = n;
+        } else if (r0 > 0) {
+            k.u0 = 0;
+            k.u1 = r0;
+            k.u_after = false;
+        }
+        k.r0 = r0;
+        k.r1 = r1;
+        return k;
+    }
+    // rank ranges of a W-way shard from the description alone: the expected
+    // in-degree (sum of |src| * p over the connections into a neuron) sets
+    // the receiving region and the receive cost, so every rank computes the
+    // same cut before (and without) building the whole graph
+    static shard_cut shard_cut_of(const network_desc& d, uint32_t W) {
+        const uint32_t n = d.neuron_count();
+        std::vector<double> e(n, 0.0);
+        for (const auto& c : d.connections) {
+            auto [sa, sb] = d.id_range(c.src);
+            auto [ta, tb] = d.id_range(c.dst);
+            if (c.p <= 0.0 || sb == sa) continue;
+            for (uint32_t t = ta; t < tb; ++t) e[t] += double(sb - sa) * c.p;
+        }
+        shard_cut k = region_of(e, n);
+        std::vector<double> prefix(size_t(k.r1 - k.r0) + 1, 0.0);
+        for (uint32_t j = 0; j < k.r1 - k.r0; ++j) prefix[j + 1] = prefix[j] + receive_cost(e[k.r0 + j]);
+        k.ra = cut_by_cost(prefix, k.r0, k.r0, k.r1, W);
+        k.ub = cut_by_count(k.u0, k.u1, W);
+        return k;
+    }
+
     // Partition for the persistent engine (detail/persistent.cuh): every CTA
     // owns a receiving piece A_c and an update-only piece B_c; pieces tile the
     // id space and are numbered in id order.
@@ -629,25 +727,15 @@ private:
         float delta[dev::kMaxClasses] = {};
         const int K = population_delivery<Model>::classes(model_, n_, bound, delta);
         if (K < 1 || K > dev::kMaxClasses || n_ == 0) return;
-        // receiving region [r0, r1): everything outside receives nothing
-        uint32_t r0 = 0, r1 = 0;
-        while (r0 < n_ && indeg[r0] == 0) ++r0;
-        r1 = n_;
-        while (r1 > r0 && indeg[r1 - 1] == 0) --r1;
-        if (r0 == r1) r0 = r1 = 0;
-        // the update-only remainder must be one range on one side, else the
-        // whole id space is the receiving region (B pieces stay empty)
-        uint32_t u0 = r1, u1 = n_;
-        bool u_after = true;
-        if (r0 > 0 && r1 < n_) {
-            r0 = 0;
-            r1 = n_;
-            u0 = u1 = n_;
-        } else if (r0 > 0) {
-            u0 = 0;
-            u1 = r0;
-            u_after = false;
-        }
+        // receiving region [r0, r1): everything outside receives nothing.
+        // A shard only holds its own sub-rows, so its region and rank ranges
+        // come from the description (shard_cut_of, identical on every rank);
+        // the CTA cut inside the rank uses the exact local in-degrees.
+        const uint32_t W = std::max<uint32_t>(1, opt_.shard_world), R = opt_.shard_rank;
+        if (R >= W) throw std::invalid_argument("shard rank out of range");
+        shard_cut cut = W > 1 ? cut_ : region_of(indeg, n_);
+        const uint32_t r0 = cut.r0, r1 = cut.r1, u0 = cut.u0, u1 = cut.u1;
+        const bool u_after = cut.u_after;
         const uint32_t nr = r1 - r0;
         const uint32_t NTH = dev::kPersistThreads;
         // ~90% thread occupancy per CTA keeps one neuron per thread (NPT = 1)
@@ -668,36 +756,18 @@ private:
         // shards: contiguous rank ranges of the receiving region (by receive
         // cost) and of the update-only region (by count); then this rank's
         // range into C local pieces of each kind
-        const uint32_t W = std::max<uint32_t>(1, opt_.shard_world), R = opt_.shard_rank;
-        if (R >= W) throw std::invalid_argument("shard rank out of range");
         std::vector<double> prefix(size_t(nr) + 1, 0.0);
-        for (uint32_t k = 0; k < nr; ++k) prefix[k + 1] = prefix[k] + 16.0 + 0.003 * indeg[r0 + k];
-        auto cut_cost = [&](uint32_t lo, uint32_t hi, uint32_t parts) {  // ids in [lo, hi) of the region
-            std::vector<uint32_t> b(parts + 1);
-            const double c0 = prefix[lo - r0], c1 = prefix[hi - r0];
-            for (uint32_t c = 0; c <= parts; ++c) {
-                const double target = c0 + (c1 - c0) * c / parts;
-                b[c] = r0 + static_cast<uint32_t>(std::lower_bound(prefix.begin(), prefix.end(), target) - prefix.begin());
-                b[c] = std::clamp(b[c], lo, hi);
-            }
-            b[0] = lo;
-            b[parts] = hi;
-            for (uint32_t c = 1; c <= parts; ++c) b[c] = std::max(b[c], b[c - 1]);
-            return b;
-        };
-        auto cut_count = [](uint32_t lo, uint32_t hi, uint32_t parts) {
-            std::vector<uint32_t> b(parts + 1);
-            for (uint32_t c = 0; c <= parts; ++c) b[c] = lo + static_cast<uint32_t>(uint64_t(hi - lo) * c / parts);
-            return b;
-        };
-        const std::vector<uint32_t> ra = cut_cost(r0, r1, W), ub = cut_count(u0, u1, W);
+        for (uint32_t k = 0; k < nr; ++k) prefix[k + 1] = prefix[k] + receive_cost(indeg[r0 + k]);
+        auto cut_cost = [&](uint32_t lo, uint32_t hi, uint32_t parts) { return cut_by_cost(prefix, r0, lo, hi, parts); };
+        const std::vector<uint32_t> ra = W > 1 ? cut.ra : std::vector<uint32_t>{r0, r1};
+        const std::vector<uint32_t> ub = W > 1 ? cut.ub : std::vector<uint32_t>{u0, u1};
         if (W > 1) {  // the local shard sizes its CTA count by its own neurons
             const uint64_t mine = (ra[R + 1] - ra[R]) + (ub[R + 1] - ub[R]);
             if (!opt_.tiles) C = tiles_for(static_cast<int64_t>(mine));
         }
         if (C + W - 1 > uint32_t(dev::kMaxTiles)) return;
         if (2ull * delay_ >= (1u << 15)) return;  // 16-bit frame tags need Q << 65536
-        const std::vector<uint32_t> alo = cut_cost(ra[R], ra[R + 1], C), blo = cut_count(ub[R], ub[R + 1], C);
+        const std::vector<uint32_t> alo = cut_cost(ra[R], ra[R + 1], C), blo = cut_by_count(ub[R], ub[R + 1], C);
         uint32_t longest = 0, wcap = 1;
         for (uint32_t c = 0; c < C; ++c) {
             longest = std::max(longest, (alo[c + 1] - alo[c]) + (blo[c + 1] - blo[c]));
@@ -1495,6 +1565,7 @@ private:
     dev_array<uint32_t> xremotes_, xsend_, xrecv_;
     void* nccl_ = nullptr;  // ncclComm_t of the in-engine exchange
     std::array<uint32_t, 4> shard_lo_{};           // this shard: A [lo, hi), B [lo, hi)
+    shard_cut cut_;                                // W > 1: rank ranges from the description
     std::vector<int64_t> imported_upto_;            // frames < this imported, per rank
     dev_array<uint32_t> xbuf_;
     dev_array<uint32_t> ibuf_[2];

@@ -152,7 +152,8 @@ construction_plan plan_jobs(const network_desc& desc, uint64_t seed, uint32_t pi
 namespace {
 
 struct dev_job {
-    uint32_t n, a, b, pad;
+    uint32_t n, a, b;
+    uint32_t nl;     // outputs inside the target range [tlo, thi) (= n for a full build)
     uint64_t o;      // final (sorted) offset of the job's first output
     uint64_t index;  // position in plan order: the stream is derive_seed(seed, index + 1)
 };
@@ -163,13 +164,25 @@ __host__ __device__ inline double tie_guard(uint32_t n, double scale) {
     return 2.0 * scale * (6.0 * (n + 2.0) + 24.0) * 0x1p-52 + 1e-12;
 }
 
-__global__ void k_expand(const dev_job* __restrict__ jobs, uint64_t njobs, uint64_t seed,
-                         uint32_t* __restrict__ cells, uint64_t* __restrict__ flagged,
-                         unsigned long long* __restrict__ nflagged, uint64_t flag_cap) {
+// mode 0: write the job's outputs inside [tlo, thi) (at most job.nl of them)
+// to cells + job.o; mode 1: count them into lcount[j] (shard sub-rows).  Jobs
+// whose range lies inside [tlo, thi) need no replay to be counted.
+__global__ void k_expand(const dev_job* __restrict__ jobs, uint64_t njobs, uint64_t seed, uint32_t tlo,
+                         uint32_t thi, int mode, uint32_t* __restrict__ cells, uint32_t* __restrict__ lcount,
+                         uint64_t* __restrict__ flagged, unsigned long long* __restrict__ nflagged,
+                         uint64_t flag_cap) {
     for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < njobs;
          j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const dev_job job = jobs[j];
-        if (job.n == 0) continue;
+        const bool inside = job.a >= tlo && job.b <= thi;
+        if (mode == 1) {
+            if (inside || job.n == 0 || job.b <= tlo || job.a >= thi) {
+                lcount[j] = inside ? job.n : 0u;
+                continue;
+            }
+        } else if (job.nl == 0) {
+            continue;
+        }
         const uint64_t stream = derive_seed(seed, job.index + 1);
         // pass 1: total = sum of the first n+1 exponentials, left to right
         xorshift r(stream);
@@ -183,14 +196,20 @@ __global__ void k_expand(const dev_job* __restrict__ jobs, uint64_t njobs, uint6
         double prefix = 0.0;
         bool close = false;
         uint32_t* out = cells + job.o;
+        uint32_t k = 0;
         for (uint32_t i = 0; i < job.n; ++i) {
             prefix += -log(r.uniform01());
             const double v = prefix / total * scale;
             const double f = floor(v + 0.5);
             const double d = (v + 0.5) - f;
             close |= (d < guard) || (1.0 - d < guard);
-            out[i] = job.a + static_cast<uint32_t>(f) + i;
+            const uint32_t t = job.a + static_cast<uint32_t>(f) + i;
+            if (t >= tlo && t < thi) {
+                if (mode == 0 && k < job.nl) out[k] = t;
+                ++k;
+            }
         }
+        if (mode == 1) lcount[j] = k;
         if (close) {
             const unsigned long long slot = atomicAdd(nflagged, 1ull);
             if (slot < flag_cap) flagged[slot] = j;
@@ -247,83 +266,22 @@ int grid_for(uint64_t work, int block) {
 
 }  // namespace
 
-device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons, uint64_t seed,
-                                 cudaStream_t stream) {
-    device_graph g;
-    g.neurons = neurons;
-    g.deg_max = plan.deg_max;
-    g.pitch = plan.row_pitch;
-    g.edges = plan.total_edges;
-    g.jobs = plan.jobs.size();
-    g.host_degree = plan.out_degree;
-    g.host_degree.resize(neurons, 0);
+namespace {
 
-    const size_t ncells = static_cast<size_t>(neurons) * g.pitch;
-    g.cells.resize(ncells);
-    g.cells.fill_bytes(0xff, stream);  // sentinel padding
-    g.degree.resize(neurons);
-    g.degree.upload(g.host_degree.data(), neurons, stream);
-
-    // final offsets: a row's non-empty jobs ordered by target-range start.
-    // A non-empty job's offset lies strictly inside its row, so o / pitch is
-    // its source; empty jobs write nothing and are dropped.
-    std::vector<dev_job> jobs;
-    jobs.reserve(plan.jobs.size());
-    for (size_t q = 0; q < plan.jobs.size(); ++q) {
-        const auto& pj = plan.jobs[q];
-        if (pj.n == 0) continue;
-        jobs.push_back(dev_job{pj.n, pj.a, pj.b, 0, pj.o, static_cast<uint64_t>(q)});
-    }
-    for (size_t q = 0; q < jobs.size();) {
-        const uint64_t row = jobs[q].o / g.pitch;
-        size_t e = q + 1;
-        while (e < jobs.size() && jobs[e].o / g.pitch == row) ++e;
-        std::stable_sort(jobs.begin() + q, jobs.begin() + e,
-                         [](const dev_job& x, const dev_job& y) { return x.a < y.a; });
-        uint64_t o = row * g.pitch;
-        for (size_t k = q; k < e; ++k) {
-            jobs[k].o = o;
-            o += jobs[k].n;
-        }
-        q = e;
-    }
-
-    dev_array<dev_job> djobs(std::max<size_t>(1, jobs.size()));
-    djobs.upload(jobs.data(), jobs.size(), stream);
-    const uint64_t flag_cap = 1u << 20;
-    dev_array<uint64_t> flagged(flag_cap);
-    dev_array<unsigned long long> nflag(1);
-    nflag.zero(stream);
-    if (!jobs.empty()) {
-        k_expand<<<grid_for(jobs.size(), 128), 128, 0, stream>>>(
-            djobs.get(), jobs.size(), seed, g.cells.get(), flagged.get(), nflag.get(), flag_cap);
-        SYNQ_CUDA(cudaGetLastError());
-    }
-    unsigned long long nf = 0;
-    nflag.download(&nf, 1, stream);
-    SYNQ_CUDA(cudaStreamSynchronize(stream));
-
-    // host fix-up of guard-flagged jobs: glibc log, the reference's exact path
-    std::vector<uint64_t> fl(std::min<unsigned long long>(nf, flag_cap));
-    flagged.download(fl.data(), fl.size(), stream);
-    SYNQ_CUDA(cudaStreamSynchronize(stream));
-    if (nf > flag_cap) {
-        // too many to list: recompute every job on the host (never expected)
-        fl.resize(jobs.size());
-        std::iota(fl.begin(), fl.end(), 0);
-    }
-    const char* prof_env = std::getenv("SYNQ_PLAN_PROFILE");
-    if (prof_env && std::atoi(prof_env) != 0)
-        std::fprintf(stderr, "expand: %zu jobs recomputed on the host\n", fl.size());
-    // independent jobs: recompute them on all host cores, then upload.  In
-    // chunks of at most kChunkWords output words (one staging buffer, one sync
-    // per chunk), so even the recompute-everything fallback stays bounded; a
-    // worker's exception (bad_alloc ...) is rethrown here, after the join, so
-    // guarded() maps it to a status instead of std::terminate
+// Recompute the listed jobs on the host with glibc (the reference's exact
+// path) on all host cores, in chunks of at most kChunkWords staged output
+// words.  emit(i, outputs) receives job fl[i]'s in-range outputs (a
+// contiguous run of the sorted job output) and the chunk's staging base; it
+// runs on the calling thread after the chunk is complete, in list order.  A
+// worker's exception (bad_alloc ...) is rethrown after the join, so guarded()
+// maps it to a status instead of std::terminate.
+template <class Emit>
+void host_recompute(const std::vector<dev_job>& jobs, const std::vector<uint64_t>& fl, uint64_t seed,
+                    uint32_t tlo, uint32_t thi, cudaStream_t stream, Emit&& emit) {
     constexpr uint64_t kChunkWords = uint64_t(1) << 24;  // 64 MB
     const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16));
     std::vector<uint32_t> stage;
-    std::vector<uint64_t> at;  // staging offset of each job of the chunk
+    std::vector<uint64_t> at, len;  // staging offset / in-range outputs of each job of the chunk
     for (size_t q0 = 0; q0 < fl.size();) {
         size_t q1 = q0;
         uint64_t words = 0;
@@ -334,6 +292,7 @@ device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons
             ++q1;
         }
         stage.resize(std::max<uint64_t>(1, words));
+        len.assign(q1 - q0, 0);
         std::atomic<size_t> next{q0};
         std::exception_ptr err;
         std::mutex err_mu;
@@ -342,7 +301,13 @@ device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons
                 for (size_t i; (i = next.fetch_add(1)) < q1;) {
                     const dev_job& job = jobs[fl[i]];
                     xorshift r(derive_seed(seed, job.index + 1));
-                    sorted_random(job.n, job.a, job.b, r, stage.data() + at[i - q0]);
+                    uint32_t* out = stage.data() + at[i - q0];
+                    sorted_random(job.n, job.a, job.b, r, out);
+                    // keep the outputs inside [tlo, thi), moved to the front
+                    const uint32_t* lo = std::lower_bound(out, out + job.n, tlo);
+                    const uint32_t* hi = std::lower_bound(lo, static_cast<const uint32_t*>(out + job.n), thi);
+                    std::memmove(out, lo, static_cast<size_t>(hi - lo) * sizeof(uint32_t));
+                    len[i - q0] = static_cast<uint64_t>(hi - lo);
                 }
             } catch (...) {
                 std::lock_guard<std::mutex> lk(err_mu);
@@ -355,20 +320,156 @@ device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons
         work();
         for (auto& th : pool) th.join();
         if (err) std::rethrow_exception(err);
-        for (size_t i = q0; i < q1; ++i) {
-            const dev_job& job = jobs[fl[i]];
-            SYNQ_CUDA(cudaMemcpyAsync(g.cells.get() + job.o, stage.data() + at[i - q0], job.n * sizeof(uint32_t),
-                                      cudaMemcpyHostToDevice, stream));
-        }
+        for (size_t i = q0; i < q1; ++i) emit(i, stage.data() + at[i - q0], len[i - q0]);
         SYNQ_CUDA(cudaStreamSynchronize(stream));  // the staging buffer is reused by the next chunk
         q0 = q1;
     }
+}
+
+// run k_expand over `jobs` and return the guard-flagged job indices (every
+// job when more were flagged than listed: never expected)
+std::vector<uint64_t> run_expand(const dev_array<dev_job>& djobs, size_t njobs, uint64_t seed, uint32_t tlo,
+                                 uint32_t thi, int mode, uint32_t* cells, uint32_t* lcount, cudaStream_t stream) {
+    const uint64_t flag_cap = 1u << 20;
+    dev_array<uint64_t> flagged(flag_cap);
+    dev_array<unsigned long long> nflag(1);
+    nflag.zero(stream);
+    if (njobs) {
+        k_expand<<<grid_for(njobs, 128), 128, 0, stream>>>(djobs.get(), njobs, seed, tlo, thi, mode, cells, lcount,
+                                                            flagged.get(), nflag.get(), flag_cap);
+        SYNQ_CUDA(cudaGetLastError());
+    }
+    unsigned long long nf = 0;
+    nflag.download(&nf, 1, stream);
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+    std::vector<uint64_t> fl(std::min<unsigned long long>(nf, flag_cap));
+    flagged.download(fl.data(), fl.size(), stream);
+    SYNQ_CUDA(cudaStreamSynchronize(stream));
+    if (nf > flag_cap) {
+        fl.resize(njobs);
+        std::iota(fl.begin(), fl.end(), 0);
+    } else {
+        std::sort(fl.begin(), fl.end());
+    }
+    return fl;
+}
+
+}  // namespace
+
+device_graph expand_device_graph(const construction_plan& plan, uint32_t neurons, uint64_t seed,
+                                 cudaStream_t stream, uint32_t tlo, uint32_t thi, uint32_t pitch_align) {
+    thi = std::min(thi, neurons);
+    tlo = std::min(tlo, thi);
+    const bool full = tlo == 0 && thi == neurons;
+    device_graph g;
+    g.neurons = neurons;
+    g.target_lo = tlo;
+    g.target_hi = thi;
+    g.jobs = plan.jobs.size();
+
+    // a row's non-empty jobs ordered by target-range start (a source's jobs
+    // target disjoint populations, so this is the row's sorted order).  A
+    // non-empty job's plan offset lies strictly inside its row, so
+    // o / row_pitch is its source; empty jobs write nothing and are dropped,
+    // and so are the jobs of a sub-row build whose range misses [tlo, thi).
+    std::vector<dev_job> jobs;
+    std::vector<uint32_t> row_of;
+    jobs.reserve(plan.jobs.size());
+    for (size_t q = 0; q < plan.jobs.size(); ++q) {
+        const auto& pj = plan.jobs[q];
+        if (pj.n == 0 || pj.b <= tlo || pj.a >= thi) continue;
+        jobs.push_back(dev_job{pj.n, pj.a, pj.b, pj.n, 0, static_cast<uint64_t>(q)});
+        row_of.push_back(static_cast<uint32_t>(pj.o / plan.row_pitch));
+    }
+    std::vector<size_t> order(jobs.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+        return row_of[x] != row_of[y] ? row_of[x] < row_of[y] : jobs[x].a < jobs[y].a;
+    });
+    {
+        std::vector<dev_job> sj(jobs.size());
+        std::vector<uint32_t> sr(jobs.size());
+        for (size_t k = 0; k < order.size(); ++k) {
+            sj[k] = jobs[order[k]];
+            sr[k] = row_of[order[k]];
+        }
+        jobs.swap(sj);
+        row_of.swap(sr);
+    }
+    dev_array<dev_job> djobs(std::max<size_t>(1, jobs.size()));
+    const char* prof_env = std::getenv("SYNQ_PLAN_PROFILE");
+    const bool prof = prof_env && std::atoi(prof_env) != 0;
+
+    g.host_degree.assign(neurons, 0);
+    if (full) {
+        g.host_degree = plan.out_degree;
+        g.host_degree.resize(neurons, 0);
+        g.deg_max = plan.deg_max;
+        g.pitch = plan.row_pitch;
+        g.edges = plan.total_edges;
+    } else {
+        // sub-rows of a shard: count each job's outputs inside
+        // [tlo, thi) on the device (exact for jobs inside the range; guard-
+        // flagged straddling jobs are recounted on the host with glibc)
+        djobs.upload(jobs.data(), jobs.size(), stream);
+        dev_array<uint32_t> lcount(std::max<size_t>(1, jobs.size()));
+        const std::vector<uint64_t> fl =
+            run_expand(djobs, jobs.size(), seed, tlo, thi, 1, nullptr, lcount.get(), stream);
+        std::vector<uint32_t> nl(jobs.size());
+        lcount.download(nl.data(), nl.size(), stream);
+        SYNQ_CUDA(cudaStreamSynchronize(stream));
+        host_recompute(jobs, fl, seed, tlo, thi, stream,
+                       [&](size_t i, const uint32_t*, uint64_t n) { nl[fl[i]] = static_cast<uint32_t>(n); });
+        if (prof) std::fprintf(stderr, "expand [%u, %u): %zu jobs recounted on the host\n", tlo, thi, fl.size());
+        size_t w = 0;
+        for (size_t k = 0; k < jobs.size(); ++k) {
+            if (nl[k] == 0) continue;
+            jobs[w] = jobs[k];
+            jobs[w].nl = nl[k];
+            row_of[w] = row_of[k];
+            g.host_degree[row_of[k]] += nl[k];
+            g.edges += nl[k];
+            ++w;
+        }
+        jobs.resize(w);
+        row_of.resize(w);
+        for (uint32_t d : g.host_degree) g.deg_max = std::max(g.deg_max, d);
+        const uint32_t align = std::max<uint32_t>(1, pitch_align);
+        g.pitch = (g.deg_max + align - 1) / align * align;
+    }
+    // final offsets: the jobs of a row back to back
+    for (size_t q = 0; q < jobs.size();) {
+        size_t e = q + 1;
+        while (e < jobs.size() && row_of[e] == row_of[q]) ++e;
+        uint64_t o = static_cast<uint64_t>(row_of[q]) * g.pitch;
+        for (size_t k = q; k < e; ++k) {
+            jobs[k].o = o;
+            o += jobs[k].nl;
+        }
+        q = e;
+    }
+
+    const size_t ncells = static_cast<size_t>(neurons) * g.pitch;
+    g.cells.resize(std::max<size_t>(1, ncells));
+    g.cells.fill_bytes(0xff, stream);  // sentinel padding
+    g.degree.resize(std::max<uint32_t>(1, neurons));
+    g.degree.upload(g.host_degree.data(), neurons, stream);
+    djobs.upload(jobs.data(), jobs.size(), stream);
+    const std::vector<uint64_t> fl =
+        run_expand(djobs, jobs.size(), seed, tlo, thi, 0, g.cells.get(), nullptr, stream);
+    if (prof) std::fprintf(stderr, "expand: %zu jobs recomputed on the host\n", fl.size());
+    // host fix-up of guard-flagged jobs: glibc log, the reference's exact path
+    host_recompute(jobs, fl, seed, tlo, thi, stream, [&](size_t i, const uint32_t* out, uint64_t n) {
+        const dev_job& job = jobs[fl[i]];
+        if (n != job.nl) throw std::logic_error("expand: host recount differs from the job's sub-row count");
+        SYNQ_CUDA(cudaMemcpyAsync(g.cells.get() + job.o, out, n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    });
     g.tie_fixups = fl.size();
     return g;
 }
 
 device_graph build_device_graph(const network_desc& desc, uint64_t seed, uint32_t pitch_align,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, uint32_t tlo, uint32_t thi) {
     // both plans are identical; pick the cheaper: the host spends ~5.5 ns per
     // master-stream draw (m p + 1 per job), the device walk ~1 us per job
     // (B200: Brunel 1e9 11.6 s host vs 0.32 s device; 604k tiny jobs 0.07 s
@@ -384,7 +485,7 @@ device_graph build_device_graph(const network_desc& desc, uint64_t seed, uint32_
     const bool on_host = host ? std::atoi(host) != 0 : draws * 5.5e-9 < jobs * 1.0e-6 + 2e-3;
     return expand_device_graph(on_host ? plan_jobs(desc, seed, pitch_align)
                                        : plan_jobs_device(desc, seed, pitch_align, stream),
-                               desc.neuron_count(), seed, stream);
+                               desc.neuron_count(), seed, stream, tlo, thi, pitch_align);
 }
 
 adjacency_list download_graph(const device_graph& g, cudaStream_t stream) {
@@ -397,6 +498,7 @@ adjacency_list download_graph(const device_graph& g, cudaStream_t stream) {
 device_graph upload_graph(const adjacency_list& adj, cudaStream_t stream) {
     device_graph g;
     g.neurons = adj.neuron_count();
+    g.target_hi = g.neurons;
     g.deg_max = adj.deg_max();
     g.pitch = adj.row_pitch();
     g.edges = adj.edge_count();
@@ -498,7 +600,7 @@ void build_window_bitmaps(const device_graph& g, const std::vector<uint32_t>& wi
 
 adjacency_list expand_jobs(const construction_plan& plan, uint32_t neurons, uint64_t seed,
                            thread_pool*) {
-    device_graph g = expand_device_graph(plan, neurons, seed, nullptr);
+    device_graph g = expand_device_graph(plan, neurons, seed, nullptr, 0, neurons, 32);
     return download_graph(g, nullptr);
 }
 
