@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="synq", choices=["synq", "reference"])
     ap.add_argument("--synapses", type=float, default=1e9)
+    ap.add_argument("--workload", default="weak", choices=["weak", "b8"],
+                    help="N>1: 'weak' = one network of N x --synapses (weak scaling); 'b8' = BASELINE "
+                         "config 5, one Brunel network of 1.2e10 synapses over the N GPUs (strong scaling)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-steps", type=int, default=1000)
@@ -489,7 +492,8 @@ def run_sharded(args, rank, world, local):
     import paper_1912_07423_b200 as synq
     from paper_1912_07423_b200 import shard
 
-    total = int(args.synapses * world)
+    b8 = args.workload == "b8"
+    total = int(1.2e10) if b8 else int(args.synapses * world)
     in_engine = args.backend == "nccl"
     t_setup = time.perf_counter()
     if in_engine:
@@ -578,10 +582,16 @@ def run_sharded(args, rank, world, local):
     mx = torch.tensor([secs, e2e_s, ker1 - ker0], dtype=torch.float64, device=dev)
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     sm = torch.tensor([c1["deliveries"] - c0["deliveries"], c1["spikes"] - c0["spikes"], e2e_ev, l1 - l0,
-                       (d1b - d0b) + gathered], dtype=torch.float64, device=dev)
+                       (d1b - d0b) + gathered, sim.synapses], dtype=torch.float64, device=dev)
+    # each rank stores only its own targets' sub-rows: the network's synapses
+    # are the sum over ranks, the largest per-GPU share is reported beside it
+    ms = torch.tensor([sim.synapses], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    max_syn = int(ms.item())
     dist.all_reduce(sm, op=dist.ReduceOp.SUM)
     secs, e2e_s, kern = (float(x) for x in mx.tolist())
-    events, spikes, e2e_events, launches, d2h = (float(x) for x in sm.tolist())
+    events, spikes, e2e_events, launches, d2h, total_syn = (float(x) for x in sm.tolist())
+    total_syn = int(total_syn)
     if rank != 0:
         ss.close()
         return 0
@@ -595,9 +605,10 @@ def run_sharded(args, rank, world, local):
     line = {
         "metric": METRIC, "value": events / secs, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1000.0, "wall_s_per_bio_s": secs / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if b8 else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: Brunel network built on device from seed %d (reference RNG streams)" % args.seed,
-        "config": {"workload": f"brunel_{world}x1e9_sharded", "synapses": sim.synapses, "neurons": n,
+        "config": {"workload": "brunel_1.2e10_sharded (BASELINE config 5)" if b8 else f"brunel_{world}x1e9_sharded",
+                   "synapses": total_syn, "neurons": n, "synapses_per_gpu_max": max_syn,
                    "bio_s_per_step": 1.0, "dt_ms": 0.1, "delay_steps": sim.delay,
                    "parallelism": f"shard{world} (target-partitioned; " + (
                        f"in-engine ncclAllGather of spike bitmasks every {sim.delay - 1} steps)" if in_engine else
