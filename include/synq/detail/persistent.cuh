@@ -101,6 +101,10 @@ struct persist_state {
     uint32_t bm_prefetch;  // stream the bitmap rows of published spikes into L2
     uint32_t stream_mode;  // bitmap delivery: barrier-free work items instead of passes
     uint32_t max_pass;     // frames per delivery pass (<= the polling warps)
+    // fold table (k_fold_table): tab[n0 * (T1 + 1) + n1] = fl-sum from +0 of
+    // n0 copies of delta[0] then n1 copies of delta[1]; nullptr: no table
+    const float* fold_tab;
+    uint32_t fold_t0, fold_t1;
 };
 
 // streaming 16-byte read of adjacency cells: read-only, no L1 allocation
@@ -142,6 +146,46 @@ SYNQ_DEV float fold_arrivals(float acc, uint32_t n, float d) {
     }
 #pragma unroll 1
     for (; n; --n) acc = acc + d;
+    return acc;
+}
+
+// the fold table: entry (n0, n1) is the reference's sequential float sum
+// starting from +0, n0 additions of d0 followed by n1 of d1 (K == 1: t1 = 0).
+// Built on the device with the same additions as fold_arrivals.
+__global__ void k_fold_table(float d0, float d1, uint32_t t0, uint32_t t1, float* tab) {
+    for (uint32_t n0 = blockIdx.x * blockDim.x + threadIdx.x; n0 <= t0; n0 += gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        for (uint32_t k = 0; k < n0; ++k) acc = acc + d0;
+        for (uint32_t n1 = 0; n1 <= t1; ++n1) {
+            tab[n0 * (t1 + 1) + n1] = acc;
+            acc = acc + d1;
+        }
+    }
+}
+
+// fold one frame's arrival counts a[0..K) into acc in class order.  When acc
+// is zero (the LIF models reset it every step) and the table covers them, the
+// first two classes are one table read: for d != 0, (+-0) + d == d, so the
+// sequence from either zero is the table's (a zero count leaves acc alone).
+template <class M>
+SYNQ_DEV float fold_frame(const persist_state<M>& ps, float acc, const uint32_t* a) {
+    int k0 = 0;
+    if (ps.fold_tab && acc == 0.0f && (a[0] | (ps.K > 1 ? a[1] : 0u))) {
+        uint32_t n0 = a[0], n1 = ps.K > 1 ? a[1] : 0u;
+        if (n0 <= ps.fold_t0) {
+            const uint32_t m1 = min(n1, ps.fold_t1);
+            acc = __ldg(ps.fold_tab + n0 * (ps.fold_t1 + 1) + m1);
+            acc = fold_arrivals(acc, n1 - m1, ps.delta[1 % kMaxClasses]);
+            k0 = 2;
+        } else {
+            acc = __ldg(ps.fold_tab + ps.fold_t0 * (ps.fold_t1 + 1));
+            acc = fold_arrivals(acc, n0 - ps.fold_t0, ps.delta[0]);
+            k0 = 1;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxClasses; ++k)
+        if (k >= k0 && k < ps.K && a[k]) acc = fold_arrivals(acc, a[k], ps.delta[k]);
     return acc;
 }
 

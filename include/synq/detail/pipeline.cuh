@@ -273,15 +273,13 @@ __global__ void __launch_bounds__(NT, 1)
                     values_t<NF> vl;
                     load_all(ps.nf, i, vl);
                     if (j < na) {  // receiving neuron: fold frame rel s in class order
-                        float acc = detail::pack_get<ACC>::get(vl);
-                        for (int k = 0; k < ps.K; ++k) {
-                            const uint32_t a = cslot[k * ps.win_cap + j];
-                            if (a) {
-                                cslot[k * ps.win_cap + j] = 0;
-                                acc = fold_arrivals(acc, a, ps.delta[k]);
-                            }
+                        uint32_t a[kMaxClasses];
+#pragma unroll
+                        for (int k = 0; k < kMaxClasses; ++k) {
+                            a[k] = k < ps.K ? cslot[k * ps.win_cap + j] : 0u;
+                            if (a[k]) cslot[k * ps.win_cap + j] = 0;
                         }
-                        detail::pack_get<ACC>::get(vl) = acc;
+                        detail::pack_get<ACC>::get(vl) = fold_frame(ps, detail::pack_get<ACC>::get(vl), a);
                     }
                     xorshift rl;
                     bool ll = false;
@@ -365,9 +363,7 @@ __global__ void __launch_bounds__(NT, 1)
             }
             if (any) {
                 auto* accp = &ps.nf.template get<ACC>()[alo + j];
-                float acc = *accp;
-                for (int k = 0; k < ps.K; ++k) acc = fold_arrivals(acc, a[k], ps.delta[k]);
-                *accp = acc;
+                *accp = fold_frame(ps, *accp, a);
             }
         }
         if (tid == 0 && my_spikes) atomicAdd(&ps.counters[C_SPIKES], my_spikes);
@@ -384,6 +380,20 @@ __global__ void __launch_bounds__(NT, 1)
             const uint32_t j = tid + r * UT;
             if (j < na + nb) load_all(ps.nf, id_of(j), v[r]);
         }
+        // per register slot: lanes of this (warp, r) in the A piece (a lane
+        // prefix), whether this lane's neuron exists / is measured, its id
+        unsigned amask[NPT > 0 ? NPT : 1];
+        bool inmeas[NPT > 0 ? NPT : 1];
+        uint32_t ids[NPT > 0 ? NPT : 1];
+#pragma unroll
+        for (int r = 0; r < NPT; ++r) {
+            const int na_here = static_cast<int>(na) - static_cast<int>(warp * 32 + r * UT);
+            amask[r] = na_here >= 32 ? 0xffffffffu : (na_here <= 0 ? 0u : (1u << na_here) - 1u);
+            const uint32_t j = tid + r * UT;
+            ids[r] = j < na + nb ? id_of(j) : 0u;
+            inmeas[r] = j < na + nb && ids[r] >= ps.meas_lo && ids[r] < ps.meas_hi;
+        }
+        const unsigned below = (1u << lane) - 1u;
         unsigned long long my_spikes = 0;
         uint32_t slot = static_cast<uint32_t>(t0 % ps.Q);
         for (uint32_t s = 0; s < nrel; ++s, slot = slot + 1 == ps.Q ? 0u : slot + 1) {
@@ -399,25 +409,22 @@ __global__ void __launch_bounds__(NT, 1)
             mark(P_POLL);
             uint32_t* cslot = ring + (s % R) * ps.K * ps.win_cap;
             bool spk[NPT > 0 ? NPT : 1];
+            unsigned bal[NPT > 0 ? NPT : 1];
             uint32_t mcount = 0;
 #pragma unroll
             for (int r = 0; r < NPT; ++r) {
                 const uint32_t j = tid + r * UT;
                 spk[r] = false;
                 if (j < na + nb) {
-                    const uint32_t i = id_of(j);
+                    const uint32_t i = ids[r];
                     if (j < na) {  // receiving neuron: fold frame rel s in class order
-                        float acc = detail::pack_get<ACC>::get(v[r]);
                         uint32_t a[kMaxClasses];
 #pragma unroll
-                        for (int k = 0; k < kMaxClasses; ++k) a[k] = k < ps.K ? cslot[k * ps.win_cap + j] : 0u;
-#pragma unroll
-                        for (int k = 0; k < kMaxClasses; ++k)
-                            if (a[k]) {
-                                cslot[k * ps.win_cap + j] = 0;
-                                acc = fold_arrivals(acc, a[k], ps.delta[k]);
-                            }
-                        detail::pack_get<ACC>::get(v[r]) = acc;
+                        for (int k = 0; k < kMaxClasses; ++k) {
+                            a[k] = k < ps.K ? cslot[k * ps.win_cap + j] : 0u;
+                            if (a[k]) cslot[k * ps.win_cap + j] = 0;
+                        }
+                        detail::pack_get<ACC>::get(v[r]) = fold_frame(ps, detail::pack_get<ACC>::get(v[r]), a);
                     }
                     values_t<NF> vl = v[r];
                     xorshift rl = rr[r];
@@ -427,18 +434,14 @@ __global__ void __launch_bounds__(NT, 1)
                     v[r] = vl;
                     rr[r] = rl;
                     live[r] = ll;
-                    if (spk[r] && i >= ps.meas_lo && i < ps.meas_hi) ++mcount;
                 }
-                // lanes of this (warp, r) in the A piece: a lane prefix
-                const int na_here = static_cast<int>(na) - static_cast<int>(warp * 32 + r * UT);
-                const unsigned amask = na_here >= 32 ? 0xffffffffu : (na_here <= 0 ? 0u : (1u << na_here) - 1u);
-                const unsigned bal = __ballot_sync(0xffffffffu, spk[r]);
+                bal[r] = __ballot_sync(0xffffffffu, spk[r]);
+                mcount += __popc(__ballot_sync(0xffffffffu, spk[r] && inmeas[r]));
                 if (lane == 0) {
-                    s_wa[r * UW + warp] = __popc(bal & amask);
-                    s_wb[r * UW + warp] = __popc(bal & ~amask);
+                    s_wa[r * UW + warp] = __popc(bal[r] & amask[r]);
+                    s_wb[r * UW + warp] = __popc(bal[r] & ~amask[r]);
                 }
             }
-            for (int o = 16; o; o >>= 1) mcount += __shfl_xor_sync(0xffffffffu, mcount, o);
             if (lane == 0) s_mw[warp] = mcount;
             mark(P_UPDATE);
             named_bar(BAR_U, UT);  // counts and the slot zeroing are complete
@@ -479,16 +482,11 @@ __global__ void __launch_bounds__(NT, 1)
             mark(9);
 #pragma unroll
             for (int r = 0; r < NPT; ++r) {
-                const uint32_t j = tid + r * UT;
-                const int na_here = static_cast<int>(na) - static_cast<int>(warp * 32 + r * UT);
-                const unsigned amask = na_here >= 32 ? 0xffffffffu : (na_here <= 0 ? 0u : (1u << na_here) - 1u);
-                const unsigned bal = __ballot_sync(0xffffffffu, spk[r]);
-                const unsigned below = (1u << lane) - 1u;
                 if (spk[r]) {
-                    if (j < na)
-                        qslot[alo + s_wa[r * UW + warp] + __popc(bal & amask & below)] = id_of(j);
+                    if ((amask[r] >> lane) & 1u)
+                        qslot[alo + s_wa[r * UW + warp] + __popc(bal[r] & amask[r] & below)] = ids[r];
                     else
-                        qslot[blo + s_wb[r * UW + warp] + __popc(bal & ~amask & below)] = id_of(j);
+                        qslot[blo + s_wb[r * UW + warp] + __popc(bal[r] & ~amask[r] & below)] = ids[r];
                 }
             }
             const uint32_t outa = s_out[0], outb = s_out[1], meas = s_out[2];
@@ -505,7 +503,7 @@ __global__ void __launch_bounds__(NT, 1)
                 for (int r = 0; r < NPT; ++r)
                     if (spk[r])
                         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                         ps.bm + static_cast<uint64_t>(id_of(tid + r * UT)) * ps.bm_row4),
+                                         ps.bm + static_cast<uint64_t>(ids[r]) * ps.bm_row4),
                                      "r"(ps.bm_row4 * 16)
                                      : "memory");
             } else if (ps.pf_cap) {
@@ -542,9 +540,10 @@ __global__ void __launch_bounds__(NT, 1)
             if (j < na) {
                 wait_at_least(&s_delivered, nrel);
                 const uint32_t* cslot = ring + (nrel % R) * ps.K * ps.win_cap;
-                float acc = detail::pack_get<ACC>::get(v[r]);
-                for (int k = 0; k < ps.K; ++k) acc = fold_arrivals(acc, cslot[k * ps.win_cap + j], ps.delta[k]);
-                detail::pack_get<ACC>::get(v[r]) = acc;
+                uint32_t a[kMaxClasses];
+#pragma unroll
+                for (int k = 0; k < kMaxClasses; ++k) a[k] = k < ps.K ? cslot[k * ps.win_cap + j] : 0u;
+                detail::pack_get<ACC>::get(v[r]) = fold_frame(ps, detail::pack_get<ACC>::get(v[r]), a);
             }
             const uint32_t i = id_of(j);
             store_all(ps.nf, i, v[r]);

@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -862,6 +863,22 @@ private:
         win_cap_ = wcap;
         smem_ = smem;
         persistent_ = true;
+        // fold table (persistent.cuh fold_frame): the first two classes' sums
+        // from zero in one read; SYNQ_FOLD_TABLE=0 disables it
+        {
+            const char* e = std::getenv("SYNQ_FOLD_TABLE");
+            const bool want = !e || std::atoi(e) != 0;
+            const bool ok = delta_[0] != 0.0f && std::isfinite(delta_[0]) &&
+                            (K == 1 || (delta_[1] != 0.0f && std::isfinite(delta_[1])));
+            if (want && ok) {
+                fold_t0_ = 63;
+                fold_t1_ = K > 1 ? 31 : 0;
+                fold_tab_.resize(size_t(fold_t0_ + 1) * (fold_t1_ + 1));
+                dev::k_fold_table<<<1, 64, 0, stream_>>>(delta_[0], K > 1 ? delta_[1] : 0.0f, fold_t0_, fold_t1_,
+                                                         fold_tab_.get());
+                SYNQ_CUDA(cudaGetLastError());
+            }
+        }
     }
 
     // fixed-size bitmask exchange (detail/persistent.cuh k_export_bits /
@@ -1182,6 +1199,9 @@ private:
         p.K = K_;
         std::copy(bound_, bound_ + dev::kMaxClasses, p.bound);
         std::copy(delta_, delta_ + dev::kMaxClasses, p.delta);
+        p.fold_tab = fold_tab_ ? fold_tab_.get() : nullptr;
+        p.fold_t0 = fold_t0_;
+        p.fold_t1 = fold_t1_;
         p.dt = dt_;
         p.delay = delay_;
         p.counters = counters_dev_.get();
@@ -1556,6 +1576,8 @@ private:
     int K_ = 0;
     uint32_t bound_[dev::kMaxClasses] = {};
     float delta_[dev::kMaxClasses] = {};
+    dev_array<float> fold_tab_;
+    uint32_t fold_t0_ = 0, fold_t1_ = 0;
     uint32_t win_cap_ = 0, pieces_ = 0, publishers_ = 0, stage_items_ = 0;
     dev_array<uint32_t> piece_src_;
     // shard exchange
