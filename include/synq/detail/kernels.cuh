@@ -25,6 +25,7 @@
 // the step's last kernel, so one captured graph replays for any step.
 #include <cuda_runtime.h>
 
+#include <concepts>
 #include <cstdint>
 
 #include "synq/detail/device_refs.cuh"
@@ -76,6 +77,7 @@ struct engine_state {
 
     unsigned long long* counters;
     unsigned long long* tile_status;  // decoupled look-back, one word per id tile
+    uint32_t* tile_bal;               // k_update<.., false>: spike ballot per (tile, warp)
     uint32_t* tile_ctr;               // [2] dynamic tile ids, by step parity
     uint32_t* done_ctr;               // last-block detection of the step's final kernel
 
@@ -110,7 +112,7 @@ template <class M>
 SYNQ_DEV bool hist_bit(const engine_state<M>& st, uint32_t id, int64_t u) {
     if (u < 0) return false;
     const uint32_t slots = 64u * st.hist_words;
-    const uint32_t slot = static_cast<uint32_t>(u % slots);
+    const uint32_t slot = st.hist_words == 1 ? static_cast<uint32_t>(u & 63) : static_cast<uint32_t>(u % slots);
     return (st.hist[static_cast<uint64_t>(id) * st.hist_words + (slot >> 6)] >> (slot & 63)) & 1ull;
 }
 
@@ -228,7 +230,11 @@ __global__ void k_init_synapses(M model, engine_state<M> st) {
 }
 
 // ------------------------------------------------------------- update
-template <class M, int BLOCK>
+// kLookback: compact in the same kernel with a decoupled look-back across
+// tiles (large networks); otherwise every tile stores its warps' spike
+// ballots (tile_bal) and k_compact places the ids (a look-back over a few
+// hundred tiles is a chain of L2 round trips: ~10 us at Brunel+ 1e8)
+template <class M, int BLOCK, bool kLookback = true>
 __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
     using NF = typename M::neuron_fields;
     constexpr bool kSyn = synapse_fields_of<M>::present;
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
     const int64_t t = *st.t_dev;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
-        s_tile = atomicAdd(&st.tile_ctr[t & 1], 1u);
+        s_tile = kLookback ? atomicAdd(&st.tile_ctr[t & 1], 1u) : blockIdx.x;
         s_meas = 0;
     }
     __syncthreads();
@@ -260,7 +266,8 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
         if constexpr (model_uses_rng<M>())
             if (live) st.rng[i] = r;
         if (st.track_bits) {
-            const uint32_t slot = static_cast<uint32_t>(t % (64u * st.hist_words));
+            const uint32_t slot = st.hist_words == 1 ? static_cast<uint32_t>(t & 63)
+                                                     : static_cast<uint32_t>(t % (64u * st.hist_words));
             uint64_t* w = st.hist + static_cast<uint64_t>(i) * st.hist_words + (slot >> 6);
             *w = (*w & ~(1ull << (slot & 63))) | (static_cast<uint64_t>(spk) << (slot & 63));
         }
@@ -279,6 +286,15 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
     const bool meas = spk && i >= st.meas_lo && i < st.meas_hi;
     const unsigned mball = __ballot_sync(0xffffffffu, meas);
     if (lane == 0 && mball) atomicAdd(&s_meas, __popc(mball));
+    if constexpr (!kLookback) {
+        if (lane == 0) st.tile_bal[tile * NW + warp] = ball;
+        __syncthreads();
+        if (threadIdx.x == 0 && s_meas) {
+            const int64_t rel = t - *st.t0_dev;
+            if (rel < st.step_cap) atomicAdd(&st.step_meas[rel], s_meas);
+        }
+        return;
+    }
     __syncthreads();
     if (warp == 0) {
         const uint32_t c = lane < NW ? s_warp[lane] : 0;
@@ -317,6 +333,94 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
             const unsigned long long at = st.log_cursor[t & 1] + pos;
             if (at < st.log_cap) st.log[at] = i;
         }
+    }
+}
+
+// ordered placement of the spikes of step t from the tiles' ballots: tile
+// b's base is the spike count of tiles 0..b-1 (summed by the block from the
+// ballots), its warps' offsets follow, so frame t is in ascending id order
+// (a device function: run by the first ntiles blocks of the calling grid,
+// whose block size must be BLOCK)
+template <class M, int BLOCK>
+SYNQ_DEV void compact_tiles(const engine_state<M>& st, int64_t t) {
+    constexpr int NW = BLOCK / 32;
+    __shared__ uint32_t s_red[NW], s_warp[NW];
+    __shared__ uint32_t s_base;
+    const uint32_t ntiles = (st.n + BLOCK - 1) / BLOCK;
+    if (blockIdx.x >= ntiles) return;
+    const uint32_t tile = blockIdx.x, lane = lane_id(), warp = threadIdx.x >> 5;
+    uint32_t before = 0;
+    for (uint32_t w = threadIdx.x; w < tile * NW; w += BLOCK) before += __popc(st.tile_bal[w]);
+    for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    if (lane == 0) s_red[warp] = before;
+    const unsigned ball = st.tile_bal[tile * NW + warp];
+    if (lane == 0) s_warp[warp] = __popc(ball);
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t b = lane < NW ? s_red[lane] : 0u;
+        for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+        const uint32_t c = lane < NW ? s_warp[lane] : 0u;
+        uint32_t incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        if (lane < NW) s_warp[lane] = incl - c;
+        const uint32_t agg = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 0) {
+            s_base = b;
+            if (tile == ntiles - 1) {  // the last tile knows the frame size
+                const uint32_t total = b + agg;
+                const int64_t rel = t - *st.t0_dev;
+                st.qcount[t % st.Q] = total;
+                atomicAdd(&st.counters[C_SPIKES], total);
+                if (rel < st.step_cap) st.step_spikes[rel] = total;
+                if (st.log) {
+                    const unsigned long long base = st.log_cursor[t & 1];
+                    st.log_cursor[(t + 1) & 1] = base + total;
+                    if (base + total > st.log_cap) st.flags[0] = 1;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if ((ball >> lane) & 1u) {
+        const uint32_t i = tile * BLOCK + threadIdx.x;
+        const uint32_t pos = s_base + s_warp[warp] + __popc(ball & ((1u << lane) - 1u));
+        st.queue[static_cast<uint64_t>(t % st.Q) * st.n + pos] = i;
+        if (st.log) {
+            const unsigned long long at = st.log_cursor[t & 1] + pos;
+            if (at < st.log_cap) st.log[at] = i;
+        }
+    }
+}
+
+template <class M, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_compact(engine_state<M> st) {
+    compact_tiles<M, BLOCK>(st, *st.t_dev);
+}
+
+// debug_checks (engine.hpp:440-446 check_frame): frame t of the generic
+// engine is strictly ascending (sorted, unique) and, with the bit history,
+// its size equals the popcount of the history slot.  flags[3] |= 1 (order)
+// or 2 (popcount); the host throws the reference's logic_error messages.
+template <class M>
+__global__ void k_check_frame(engine_state<M> st) {
+    __shared__ unsigned long long s_pop;
+    const int64_t t = *st.t_dev;
+    const uint32_t cnt = st.qcount[t % st.Q];
+    const uint32_t* f = st.queue + static_cast<uint64_t>(t % st.Q) * st.n;
+    if (threadIdx.x == 0) s_pop = 0;
+    __syncthreads();
+    bool bad = false;
+    for (uint32_t i = threadIdx.x + 1; i < cnt; i += blockDim.x) bad |= f[i - 1] >= f[i];
+    if (bad) atomicOr(st.flags + 3, 1u);
+    if (st.track_bits) {
+        unsigned long long pop = 0;
+        for (uint32_t i = threadIdx.x; i < st.n; i += blockDim.x) pop += hist_bit(st, i, t) ? 1 : 0;
+        atomicAdd(&s_pop, pop);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_pop != cnt) atomicOr(st.flags + 3, 2u);
     }
 }
 
@@ -395,6 +499,160 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
     }
 }
 
+// Catch-up for one-word histories (history <= 64 steps, the default 50):
+// the replay window [a0, through] is at most 64 steps, so the pre and post
+// bits of the whole window are two register words rotated to start at a0;
+// between events the model is stepped with (false, false) in a tight loop
+// (for STDP: two multiplies per step).  A model exposing
+// plastic(src, dst) declares update_synapse a no-op for the other synapses
+// (benchmarks.hpp brunel_plus_model), which are skipped.  Same results as
+// k_catchup, bit for bit.
+template <class M>
+constexpr bool model_has_plastic() {
+    return requires(const M& m, uint32_t a, uint32_t b) { { m.plastic(a, b) } -> std::convertible_to<bool>; };
+}
+SYNQ_DEV uint64_t rotr64(uint64_t x, uint32_t r) { return r ? (x >> r) | (x << (64 - r)) : x; }
+
+// the catch-up list of step t: frame(due) U expiring (mode 0), or every
+// neuron (mode 1, flush through t - 1)
+template <class M>
+struct catchup_list {
+    const uint32_t* frame = nullptr;
+    uint32_t ntr = 0, total = 0;
+    int64_t through = 0;
+    SYNQ_DEV void load(const engine_state<M>& st, int mode, int64_t t) {
+        through = mode == 0 ? t : t - 1;
+        if (mode == 0) {
+            const int64_t due = t - static_cast<int64_t>(st.delay) + 1;
+            if (due >= 0) {
+                frame = st.queue + static_cast<uint64_t>(due % st.Q) * st.n;
+                ntr = st.qcount[due % st.Q];
+            }
+            total = ntr + *st.expiring_count;
+        } else {
+            total = st.n;
+            ntr = 0;
+            frame = nullptr;
+        }
+    }
+    SYNQ_DEV uint32_t at(const engine_state<M>& st, int mode, uint32_t k) const {
+        return mode == 1 ? k : (k < ntr ? frame[k] : st.expiring[k - ntr]);
+    }
+};
+
+// ages of the caught-up neurons: through + 1 (engine.hpp:434); strided over
+// the calling grid (after every catch-up item of the step has run)
+template <class M>
+SYNQ_DEV void advance_ages(const engine_state<M>& st, const catchup_list<M>& cl, int mode) {
+    for (uint32_t kq = blockIdx.x * blockDim.x + threadIdx.x; kq < cl.total; kq += gridDim.x * blockDim.x) {
+        const uint32_t nid = cl.at(st, mode, kq);
+        if (static_cast<int64_t>(st.ages[nid]) <= cl.through) st.ages[nid] = static_cast<uint32_t>(cl.through + 1);
+    }
+}
+
+// replay one synapse over n <= 64 steps from pre / post bit windows
+template <class M, class SS>
+SYNQ_DEV void replay_window(const M& model, SS& sv, uint64_t prew, uint64_t postw, uint32_t n, float dt) {
+    uint64_t ev = prew | postw;
+    uint32_t j = 0;
+    while (j < n) {
+        const uint32_t e = ev ? static_cast<uint32_t>(__ffsll(static_cast<long long>(ev))) - 1 : n;
+#pragma unroll 4
+        for (; j < e; ++j) model.update_synapse(sv, false, false, dt);
+        if (e < n) {
+            model.update_synapse(sv, ((prew >> e) & 1ull) != 0, ((postw >> e) & 1ull) != 0, dt);
+            ev &= ev - 1;
+            j = e + 1;
+        }
+    }
+}
+
+template <class M, bool kCompact = false>
+__global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st, int mode) {
+    using SF = typename synapse_fields_of<M>::type;
+    constexpr int U = 4;  // synapses per thread, loads batched
+    const int64_t t = *st.t_dev;
+    if constexpr (kCompact) compact_tiles<M, 256>(st, t);
+    catchup_list<M> cl;
+    cl.load(st, mode, t);
+    if (mode == 0 && blockIdx.x == 0 && threadIdx.x == 0 && cl.total > cl.ntr)
+        atomicAdd(&st.counters[C_EXPIRY], cl.total - cl.ntr);
+    const int64_t through = cl.through;
+    // work item = (neuron, chunk of U x 256 synapses); ages advance later
+    const uint32_t mc = (st.deg_max + U * 256 - 1) / (U * 256);
+    const uint64_t items = static_cast<uint64_t>(cl.total) * mc;
+    for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const uint32_t kq = static_cast<uint32_t>(it / mc), ch = static_cast<uint32_t>(it % mc);
+        const uint32_t nid = cl.at(st, mode, kq);
+        const int64_t a0 = st.ages[nid];
+        if (a0 > through) continue;
+        const uint32_t n = static_cast<uint32_t>(through - a0 + 1);  // <= 64 under the expiry rule
+        const uint32_t d = st.degree[nid];
+        if (ch == 0 && threadIdx.x == 0)
+            atomicAdd(&st.counters[C_SYN_UPDATES], static_cast<unsigned long long>(d) * n);
+        const uint32_t k0 = ch * U * 256 + threadIdx.x;
+        if (k0 >= d) continue;
+        const uint64_t lastn = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+        // pre bits: u - delay for u in [a0, through]; u - delay < 0 is false
+        const int64_t p0 = a0 - static_cast<int64_t>(st.delay);
+        uint64_t prew = 0;
+        if (n <= 64 && p0 + static_cast<int64_t>(n) > 0) {
+            const uint64_t hw = st.hist[nid];
+            if (p0 >= 0) {
+                prew = rotr64(hw, static_cast<uint32_t>(p0 % 64));
+            } else {
+                const uint32_t neg = static_cast<uint32_t>(-p0);  // leading steps with u - delay < 0
+                prew = neg >= 64 ? 0ull : (hw << neg);             // bit j <- slot j - neg = u - delay
+            }
+        }
+        prew &= lastn;
+        const uint32_t r0 = static_cast<uint32_t>(a0 % 64);
+        const uint32_t* row = st.cells + static_cast<uint64_t>(nid) * st.pitch;
+        uint32_t dst[U];
+        bool on[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t kk = k0 + u * 256;
+            on[u] = kk < d;
+            dst[u] = on[u] ? row[kk] : 0u;
+        }
+        synapse_state<SF> sv[U];
+        uint64_t postw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if constexpr (model_has_plastic<M>()) on[u] = on[u] && model.plastic(nid, dst[u]);
+            postw[u] = 0;
+            if (on[u]) {
+                load_syn(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 256, sv[u]);
+                postw[u] = st.hist[dst[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!on[u]) continue;
+            if constexpr (model_has_plastic<M>()) __builtin_assume(model.plastic(nid, dst[u]));
+            const synapse_state<SF> s0 = sv[u];
+            sv[u].src_ = nid;
+            sv[u].dst_ = dst[u];
+            if (n > 64) {  // not reached under the expiry rule; replayed step by step if it is
+                for (int64_t x = a0; x <= through; ++x)
+                    model.update_synapse(sv[u], hist_bit(st, nid, x - static_cast<int64_t>(st.delay)),
+                                         hist_bit(st, dst[u], x), st.dt);
+            } else {
+                replay_window(model, sv[u], prew, rotr64(postw[u], r0) & lastn, n, st.dt);
+            }
+            store_syn_changed(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 256, sv[u], s0);
+        }
+    }
+}
+
+template <class M>
+__global__ void k_catchup_ages(engine_state<M> st, int mode) {
+    catchup_list<M> cl;
+    cl.load(st, mode, *st.t_dev);
+    advance_ages(st, cl, mode);
+}
+
 // ------------------------------------------------------------- receive
 template <class M>
 SYNQ_DEV void deliver(const M& model, const engine_state<M>& st, uint32_t src, uint32_t k,
@@ -439,6 +697,285 @@ __global__ void __launch_bounds__(BLOCK) k_receive(M model, engine_state<M> st) 
         }
         for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
         if (lane == 0 && mine) atomicAdd(&st.counters[C_DELIVERIES], mine);
+    }
+    step_epilogue(st, t);
+}
+
+// ---- ordered windowed delivery (exact, the default for the generic engine)
+// CTA c owns the targets [lo[c], lo[c+1]) and keeps their state in registers
+// (thread j: targets j, j + BLOCK, ...).  Per chunk of the due frame's spikes
+// (ascending ids) it stages the spikes' row segments inside its window
+// (split[s][c] .. split[s][c+1], like the persistent engine) together with
+// the synapse state they read, buckets the events by target in ascending
+// spike order (rank = popcount of the target's spike bitmask below the
+// spike: order-free to build), and each thread then applies its targets'
+// events in that order through model.receive.  That is the reference's
+// sequential accumulation order per target (engine.hpp:384-404), so the
+// result is bit-identical to its deterministic mode, with no device atomics
+// on neuron state and no sort.
+struct recv_win {
+    const uint32_t* lo;     // [C + 1] window bounds (lo[C] = n)
+    const uint32_t* split;  // [n][C + 1] row position of the first target >= lo[c]
+    uint32_t C;
+    uint32_t wmax;  // largest window (<= kWinTPT * block)
+    uint32_t ecap;  // events staged per chunk
+    uint32_t ages;  // advance the ages of the step's k_catchup1 list first
+};
+constexpr int kWinTPT = 4;      // targets per thread
+constexpr int kWinSpikes = 256;  // spikes per chunk (8 mask words per target)
+
+// synapse handle on the staged copy of an event's synapse state
+template <class FieldList>
+struct staged_synapse {
+    uint32_t e_, src_, dst_;
+    unsigned char* base_;
+    uint32_t ecap_;
+    SYNQ_HD uint32_t src() const { return src_; }
+    SYNQ_HD uint32_t dst() const { return dst_; }
+    template <size_t I>
+    SYNQ_HD auto& get() const {
+        return reinterpret_cast<field_t<I, FieldList>*>(base_ + staged_offset<I>(ecap_))[e_];
+    }
+    template <size_t I>
+    SYNQ_HD static size_t staged_offset(uint32_t ecap) {
+        if constexpr (I == 0)
+            return 0;
+        else
+            return staged_offset<I - 1>(ecap) + ((sizeof(field_t<I - 1, FieldList>) * ecap + 15) & ~size_t(15));
+    }
+};
+template <class FieldList, size_t I = 0>
+SYNQ_DEV void stage_syn(const field_ptrs<FieldList>& f, uint64_t i, unsigned char* base, uint32_t ecap, uint32_t e) {
+    if constexpr (I < FieldList::count) {
+        using T = field_t<I, FieldList>;
+        reinterpret_cast<T*>(base + staged_synapse<FieldList>::template staged_offset<I>(ecap))[e] =
+            f.template get<I>()[i];
+        stage_syn<FieldList, I + 1>(f, i, base, ecap, e);
+    }
+}
+// staged arrays hold 2 x half entries per field: [0, half) working copies,
+// [half, 2 half) the originals
+template <class FieldList, size_t I = 0>
+SYNQ_DEV void unstage_syn(const field_ptrs<FieldList>& f, uint64_t i, const unsigned char* base, uint32_t ecap2,
+                          uint32_t e, uint32_t half) {
+    if constexpr (I < FieldList::count) {
+        using T = field_t<I, FieldList>;
+        const T* a = reinterpret_cast<const T*>(base + staged_synapse<FieldList>::template staged_offset<I>(ecap2));
+        if (!same_bits(a[e], a[e + half])) f.template get<I>()[i] = a[e];
+        unstage_syn<FieldList, I + 1>(f, i, base, ecap2, e, half);
+    }
+}
+template <class FieldList, size_t I = 0>
+SYNQ_DEV void copy_staged(unsigned char* base, uint32_t ecap2, uint32_t n) {
+    if constexpr (I < FieldList::count) {
+        using T = field_t<I, FieldList>;
+        T* a = reinterpret_cast<T*>(base + staged_synapse<FieldList>::template staged_offset<I>(ecap2));
+        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) a[e + ecap2 / 2] = a[e];
+        copy_staged<FieldList, I + 1>(base, ecap2, n);
+    }
+}
+
+template <class M, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st, recv_win rw) {
+    using NF = typename M::neuron_fields;
+    using SF = typename synapse_fields_of<M>::type;
+    constexpr bool kSyn = synapse_fields_of<M>::present;
+    constexpr int NW = BLOCK / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_spk[kWinSpikes], s_sb[kWinSpikes], s_off[kWinSpikes + 1];
+    __shared__ uint32_t s_tmp[NW + 1];
+    __shared__ uint32_t s_take;
+    const uint32_t wmax = rw.wmax, ecap = rw.ecap;
+    uint32_t* s_tcnt = reinterpret_cast<uint32_t*>(smem);  // wmax
+    uint32_t* s_toff = s_tcnt + wmax;                      // wmax
+    uint32_t* s_mask = s_toff + wmax;                      // wmax x 8
+    uint32_t* s_ev = s_mask + 8 * wmax;                    // ecap: row position k | spike << 24
+    uint32_t* s_et = s_ev + ecap;                          // ecap: local target
+    uint32_t* s_ord = s_et + ecap;                         // ecap: events by (target, spike)
+    unsigned char* s_syn = reinterpret_cast<unsigned char*>(s_ord + ecap);
+
+    const int64_t t = *st.t_dev;
+    const int64_t due = t - static_cast<int64_t>(st.delay) + 1;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t c = blockIdx.x, C = rw.C;
+    if constexpr (kSyn)
+        if (rw.ages) {
+            catchup_list<M> cl;
+            cl.load(st, 0, t);
+            advance_ages(st, cl, 0);
+        }
+    const uint32_t lo = rw.lo[c], wn = rw.lo[c + 1] - lo;
+    unsigned long long mine = 0;
+    if (due >= 0 && wn > 0) {
+        const uint32_t S = st.qcount[due % st.Q];
+        const uint32_t* spikes = st.queue + static_cast<uint64_t>(due % st.Q) * st.n;
+        values_t<NF> v[kWinTPT], v0[kWinTPT];
+        xorshift rr[kWinTPT];
+        bool live[kWinTPT];
+#pragma unroll
+        for (int r = 0; r < kWinTPT; ++r) {
+            live[r] = false;
+            const uint32_t j = tid + r * BLOCK;
+            if (j < wn) load_all(st.nf, lo + j, v[r]);
+            v0[r] = v[r];
+        }
+        for (uint32_t g0 = 0; g0 < S;) {
+            const uint32_t m = min(static_cast<uint32_t>(kWinSpikes), S - g0);
+            // (1) the spikes' segments in this window; exclusive scan of their sizes
+            uint32_t cnt = 0;
+            if (tid < m) {
+                const uint32_t sid = spikes[g0 + tid];
+                const uint32_t* sp = rw.split + static_cast<uint64_t>(sid) * (C + 1) + c;
+                const uint32_t sb = sp[0];
+                cnt = sp[1] - sb;
+                s_spk[tid] = sid;
+                s_sb[tid] = sb;
+            }
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= static_cast<uint32_t>(o)) incl += y;
+            }
+            if (lane == 31) s_tmp[warp] = incl;
+            for (uint32_t x = tid; x < wn; x += BLOCK) s_tcnt[x] = 0;
+            for (uint32_t x = tid; x < 8 * wn; x += BLOCK) s_mask[x] = 0;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t w = lane < NW ? s_tmp[lane] : 0u;
+                uint32_t wi = w;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                    if (lane >= static_cast<uint32_t>(o)) wi += y;
+                }
+                if (lane < NW) s_tmp[lane] = wi - w;
+            }
+            __syncthreads();
+            if (tid < kWinSpikes) s_off[tid + 1] = s_tmp[warp] + incl;
+            if (tid == 0) s_off[0] = 0;
+            __syncthreads();
+            // take the longest spike prefix whose events fit (at least one spike)
+            if (tid < m && s_off[tid] <= ecap && (tid + 1 == m || s_off[tid + 1] > ecap))
+                s_take = s_off[tid + 1] <= ecap ? tid + 1 : max(1u, tid);
+            __syncthreads();
+            const uint32_t mt = s_take, E = s_off[mt];
+            // (2) events, one per thread (spike found by binary search over
+            // the segment offsets), up to 4 per thread with their loads in
+            // flight together; the synapse state is staged twice (working
+            // copy + original, so write-back needs no global reads)
+            for (uint32_t e0 = 0; e0 < E; e0 += 4 * BLOCK) {
+                uint32_t ej[4], ek[4], tg[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = e0 + u * BLOCK + tid;
+                    tg[u] = 0;
+                    if (e < E) {
+                        uint32_t a = 0, z = mt;  // last j with s_off[j] <= e
+                        while (z - a > 1) {
+                            const uint32_t mid = (a + z) >> 1;
+                            if (s_off[mid] <= e)
+                                a = mid;
+                            else
+                                z = mid;
+                        }
+                        ej[u] = a;
+                        ek[u] = s_sb[a] + (e - s_off[a]);
+                        tg[u] = st.cells[static_cast<uint64_t>(s_spk[a]) * st.pitch + ek[u]];
+                        if constexpr (kSyn)
+                            stage_syn(st.sf, static_cast<uint64_t>(s_spk[a]) * st.deg_max + ek[u], s_syn, 2 * ecap, e);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = e0 + u * BLOCK + tid;
+                    if (e < E) {
+                        const uint32_t j = ej[u], tl = tg[u] - lo;
+                        s_ev[e] = ek[u] | (j << 24);
+                        s_et[e] = tl;
+                        atomicAdd(&s_tcnt[tl], 1u);
+                        atomicOr(&s_mask[tl * 8 + (j >> 5)], 1u << (j & 31));
+                    }
+                }
+            }
+            __syncthreads();
+            if constexpr (kSyn)  // original copy for the write-back comparison
+                copy_staged<SF>(s_syn, 2 * ecap, E);
+            __syncthreads();
+            // (3) target offsets (exclusive scan over the window)
+            uint32_t carry = 0;
+            for (uint32_t b0 = 0; b0 < wn; b0 += BLOCK) {
+                const uint32_t x = b0 + tid < wn ? s_tcnt[b0 + tid] : 0u;
+                uint32_t in2 = x;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, in2, o);
+                    if (lane >= static_cast<uint32_t>(o)) in2 += y;
+                }
+                if (lane == 31) s_tmp[warp] = in2;
+                __syncthreads();
+                if (warp == 0) {
+                    const uint32_t w = lane < NW ? s_tmp[lane] : 0u;
+                    uint32_t wi = w;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                        if (lane >= static_cast<uint32_t>(o)) wi += y;
+                    }
+                    if (lane < NW) s_tmp[lane] = wi - w;
+                    if (lane == 31) s_tmp[NW] = wi;
+                }
+                __syncthreads();
+                if (b0 + tid < wn) s_toff[b0 + tid] = carry + s_tmp[warp] + in2 - x;
+                carry += s_tmp[NW];
+                __syncthreads();
+            }
+            // (4) stable placement: rank = earlier spikes of this chunk hitting the target
+            for (uint32_t e = tid; e < E; e += BLOCK) {
+                const uint32_t tl = s_et[e], j = s_ev[e] >> 24;
+                const uint32_t* mk = s_mask + tl * 8;
+                uint32_t rank = __popc(mk[j >> 5] & ((1u << (j & 31)) - 1u));
+                for (uint32_t w = 0; w < (j >> 5); ++w) rank += __popc(mk[w]);
+                s_ord[s_toff[tl] + rank] = e;
+            }
+            __syncthreads();
+            // (5) apply, per target in ascending spike order
+#pragma unroll
+            for (int r = 0; r < kWinTPT; ++r) {
+                const uint32_t j = tid + r * BLOCK;
+                if (j >= wn) continue;
+                const uint32_t b = s_toff[j], ne = s_tcnt[j];
+                local_neuron<NF> to{lo + j, &v[r], &rr[r], &live[r], st.rng};
+                for (uint32_t x = b; x < b + ne; ++x) {
+                    const uint32_t e = s_ord[x], jj = s_ev[e] >> 24;
+                    const uint32_t src = s_spk[jj];
+                    global_neuron<NF, false> from{src, st.nf, st.rng};
+                    if constexpr (kSyn) {
+                        staged_synapse<SF> syn{e, src, lo + j, s_syn, 2 * ecap};
+                        model.receive(from, to, syn);
+                    } else {
+                        model.receive(from, to);
+                    }
+                }
+            }
+            __syncthreads();
+            // (6) synapse state written by receive (if any) goes back
+            if constexpr (kSyn) {
+                for (uint32_t e = tid; e < E; e += BLOCK) {
+                    const uint32_t j = s_ev[e] >> 24, k = s_ev[e] & 0xffffffu;
+                    unstage_syn(st.sf, static_cast<uint64_t>(s_spk[j]) * st.deg_max + k, s_syn, 2 * ecap, e, ecap);
+                }
+            }
+            if (tid == 0) mine += E;
+            __syncthreads();
+            g0 += mt;
+        }
+#pragma unroll
+        for (int r = 0; r < kWinTPT; ++r) {
+            const uint32_t j = tid + r * BLOCK;
+            if (j < wn) store_changed(st.nf, lo + j, v[r], v0[r]);
+        }
+        if (tid == 0 && mine) atomicAdd(&st.counters[C_DELIVERIES], mine);
     }
     step_epilogue(st, t);
 }

@@ -773,6 +773,48 @@ __global__ void k_import(persist_state<M> ps, int64_t t0, uint32_t b, const uint
     if (threadIdx.x == 0) ps.finfo[static_cast<uint64_t>(slot) * ps.E + entry] = frame_word(t0 + k, ca, cb);
 }
 
+// debug_checks for the persistent engine (engine.hpp:440-446): block k
+// checks frame t0 + k: every publisher's piece slices are strictly ascending
+// and inside their pieces (pieces tile the id space in order, so the merged
+// frame is sorted and unique), and the slices add up to the step's spike
+// count (step_spikes, this rank's CTAs).  flags[3] |= 1 / 2.
+template <class M>
+__global__ void k_check_persist(persist_state<M> ps, int64_t t0, uint32_t b) {
+    const uint32_t k = blockIdx.x;
+    if (k >= b) return;
+    const uint32_t slot = static_cast<uint32_t>((t0 + k) % ps.Q);
+    const unsigned long long* fi = ps.finfo + static_cast<uint64_t>(slot) * ps.E;
+    const uint32_t* q = ps.queue + static_cast<uint64_t>(slot) * ps.n;
+    __shared__ unsigned long long s_local;
+    if (threadIdx.x == 0) s_local = 0;
+    __syncthreads();
+    bool bad = false;
+    unsigned long long local = 0;
+    for (uint32_t p = threadIdx.x; p < ps.P; p += blockDim.x) {
+        const uint32_t src = ps.piece_src[p];
+        if ((src >> 1) >= ps.C) continue;  // remote ranks' frames are imported after the batch
+        const unsigned long long w = fi[src >> 1];
+        if (word_tag(w) != frame_tag(t0 + k)) {
+            bad = true;
+            continue;
+        }
+        const uint32_t cnt = word_half(w, src & 1), lo = ps.piece_lo[p], hi = ps.piece_lo[p + 1];
+        local += cnt;
+        if (cnt > hi - lo) {
+            bad = true;
+            continue;
+        }
+        for (uint32_t i = 0; i < cnt; ++i) {
+            const uint32_t id = q[lo + i];
+            bad |= id < lo || id >= hi || (i > 0 && q[lo + i - 1] >= id);
+        }
+    }
+    if (bad) atomicOr(ps.flags + 3, 1u);
+    atomicAdd(&s_local, local);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_local != ps.step_spikes[k]) atomicOr(ps.flags + 3, 2u);
+}
+
 // ---- in-engine exchange (NCCL allgather of fixed-size spike bitmasks) ----
 // Rank r's send block: words[0] = b, then for step k < b: wa_max + wb_max
 // words: bit i of the A part = id a_lo_r + i spiked, bit i of the B part =

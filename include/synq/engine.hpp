@@ -289,7 +289,10 @@ public:
             bool pending = false;
             // in-engine exchange: batches of at most delay-1 steps, each
             // followed by export -> ncclAllGather -> import on this stream
-            const int64_t cap = nccl_ ? std::min<int64_t>(batch_cap_, int64_t(delay_) - 1) : int64_t(batch_cap_);
+            int64_t cap = nccl_ ? std::min<int64_t>(batch_cap_, int64_t(delay_) - 1) : int64_t(batch_cap_);
+            // debug_checks: the frames of a batch are checked after it, so a
+            // batch may not outrun the queue ring (Q slots)
+            if (opt_.debug_checks) cap = std::min<int64_t>(cap, Q_);
             while (steps > 0) {
                 const int64_t b = std::min<int64_t>(steps, cap);
                 if constexpr (population_model)
@@ -313,6 +316,7 @@ public:
             pull_counters();
             if (flags_host_[1]) throw device_error("ordered delivery scratch overflow");
             if (flags_host_[2]) throw device_error("sharded run: imported frames of a different batch length");
+            check_debug_flags();
             if (log_on_ && logged_upto_ < t_ && (!sharded() || nccl_)) drain_log();
         } else {
             while (steps > 0) {
@@ -335,8 +339,7 @@ public:
         if constexpr (has_synapses) {
             push_mirrors();
             auto t0 = clock::now();
-            dev::k_catchup<Model><<<std::max<uint32_t>(1, std::min<uint32_t>(n_, uint32_t(sms_) * 8)), 256, 0, stream_>>>(
-                model_, state(), 1);
+            enqueue_catchup(1);
             SYNQ_CUDA(cudaGetLastError());
             pull_counters();
             timings_.simulate += since(t0);
@@ -377,7 +380,7 @@ public:
     bool persistent() const { return persistent_; }
     bool pipelined() const { return persistent_ && pipe_; }
     bool bitmap_delivery() const { return persistent_ && pipe_ && pipe_bm_; }
-    bool exact() const { return exact_ || persistent_; }
+    bool exact() const { return exact_ || persistent_ || (win_on_ && !atomic_recv_); }
     uint64_t construction_fixups() const { return graph_.tie_fixups; }
     // device time of all run() calls (CUDA events on the engine stream) and of
     // the dominant kernel alone; kernel launches; host<->device bytes moved
@@ -570,7 +573,7 @@ public:
                          step_ctr_dev_.bytes() + step_spikes_dev_.bytes() + step_meas_dev_.bytes();
         m.ages = has_synapses ? uint64_t(n_) * 4 : 0;
         m.expirations = has_synapses ? uint64_t(n_) * 4 : 0;
-        m.adjacency = graph_.bytes() + split_.bytes() + bm_.bytes();  // + receive-window bitmaps
+        m.adjacency = graph_.bytes() + split_.bytes() + bm_.bytes() + win_split_.bytes();  // + receive-window bitmaps
         m.synapse_fields = detail::field_bytes<synapse_fields>() * synapse_capacity();
         return m;
     }
@@ -603,6 +606,12 @@ private:
             if (hist_words_ > 4) throw std::invalid_argument("history_frames above 256 are not supported");
             hist_.resize(std::max<size_t>(1, size_t(n_) * hist_words_));
         }
+        if (!has_synapses && opt_.debug_checks) {  // debug_checks tracks spike bits for every model
+            history_ = delay_ + 1;
+            hist_words_ = (history_ + 63) / 64;
+            if (hist_words_ > 4) throw std::invalid_argument("debug_checks: delay above 255 steps is not supported");
+            hist_.resize(std::max<size_t>(1, size_t(n_) * hist_words_));
+        }
         counters_dev_.resize(dev::C_COUNT);
         tile_ctr_.resize(2);
         done_ctr_.resize(1);
@@ -612,6 +621,7 @@ private:
         log_cursor_.resize(2);
         ntiles_update_ = std::max<uint32_t>(1, (n_ + kUpdateBlock - 1) / kUpdateBlock);
         tile_status_.resize(ntiles_update_);
+        tile_bal_.resize(size_t(ntiles_update_) * (kUpdateBlock / 32));
 
         if constexpr (population_model) {
             if (opt_.persistent != 0) setup_persistent();
@@ -630,7 +640,8 @@ private:
         Q_ = persistent_ ? 2 * delay_ : delay_;
         queue_.resize(std::max<size_t>(1, size_t(Q_) * n_));
         qcount_.resize(Q_);
-        if (!persistent_ && exact_) {
+        if (!persistent_) setup_recv_win();
+        if (!persistent_ && exact_ && !win_on_) {  // scratch of the count/scan/scatter ordered receive
             det_cnt_.resize(std::max<uint32_t>(1, n_));
             det_off_.resize(std::max<uint32_t>(1, n_));
             det_fill_.resize(std::max<uint32_t>(1, n_));
@@ -642,6 +653,53 @@ private:
         step_meas_dev_.resize(2 * size_t(batch_cap_));
         step_ctr_dev_.resize(4 * size_t(batch_cap_));
         step_buf_.resize(4 * size_t(batch_cap_));
+    }
+
+    // ordered windowed receive for the generic engine (kernels.cuh
+    // k_recv_win): target windows balanced by in-degree, at most
+    // kWinTPT x kWinBlock targets each, row splits per window.  Off when the
+    // split table would be large next to the adjacency (very sparse
+    // networks) or SYNQ_WINRECV=0; SYNQ_ATOMIC_RECV=1 keeps the device-atomic
+    // k_receive for the fast (non-deterministic) mode.
+    void setup_recv_win() {
+        if (const char* e = std::getenv("SYNQ_WINRECV"); e && std::atoi(e) == 0) return;
+        if (const char* e = std::getenv("SYNQ_ATOMIC_RECV")) atomic_recv_ = std::atoi(e) != 0;
+        if (n_ == 0 || graph_.edges == 0 || graph_.deg_max >= (1u << 24) || !graph_.cells) return;
+        const uint32_t cap_t = uint32_t(dev::kWinTPT) * kWinBlock;
+        const std::vector<uint32_t> indeg = in_degrees(graph_, stream_);
+        std::vector<double> prefix(size_t(n_) + 1, 0.0);
+        for (uint32_t k = 0; k < n_; ++k) prefix[k + 1] = prefix[k] + receive_cost(indeg[k]);
+        uint32_t C = std::min<uint32_t>(n_, std::max<uint32_t>(uint32_t(sms_), (n_ + cap_t - 1) / cap_t));
+        std::vector<uint32_t> lo;
+        uint32_t wmax = 0;
+        for (;;) {
+            lo = cut_by_cost(prefix, 0, 0, n_, C);
+            wmax = 0;
+            for (uint32_t c = 0; c < C; ++c) wmax = std::max(wmax, lo[c + 1] - lo[c]);
+            if (wmax <= cap_t || C >= n_) break;
+            C = std::min<uint32_t>(n_, C + C / 4 + 1);
+        }
+        if (wmax > cap_t) return;
+        const uint64_t split_bytes = uint64_t(n_) * (C + 1) * 4;
+        if (split_bytes > std::max<uint64_t>(256ull << 20, graph_.bytes() / 4)) return;
+        int dev = 0, max_smem = 0;
+        SYNQ_CUDA(cudaGetDevice(&dev));
+        SYNQ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        auto fn = dev::k_recv_win<Model, kWinBlock>;
+        cudaFuncAttributes fa{};
+        SYNQ_CUDA(cudaFuncGetAttributes(&fa, fn));
+        const size_t avail = size_t(max_smem) - fa.sharedSizeBytes - 1024;
+        const size_t per_target = 10 * 4, per_event = 12 + 2 * detail::field_bytes<synapse_fields>() + 16;
+        if (avail <= per_target * wmax) return;
+        size_t ecap = std::min<size_t>(8192, (avail - per_target * wmax) / per_event) & ~size_t(31);
+        if (ecap < wmax || ecap < 64) return;
+        win_smem_ = per_target * wmax + 3 * 4 * ecap + 2 * detail::field_bytes<synapse_fields>() * ecap + 16 * 8;
+        SYNQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(win_smem_)));
+        win_lo_dev_.resize(C + 1);
+        win_lo_dev_.upload(lo.data(), C + 1, stream_);
+        build_splits(graph_, lo, win_split_, stream_);
+        win_ = dev::recv_win{win_lo_dev_.get(), win_split_.get(), C, wmax, static_cast<uint32_t>(ecap)};
+        win_on_ = true;
     }
 
     // ---- partition helpers (setup_persistent; shard construction)
@@ -1010,6 +1068,7 @@ private:
         s.expiring_count = expiring_count_.get();
         s.counters = counters_dev_.get();
         s.tile_status = tile_status_.get();
+        s.tile_bal = tile_bal_.get();
         s.tile_ctr = tile_ctr_.get();
         s.done_ctr = done_ctr_.get();
         s.t_dev = t_dev_.get();
@@ -1026,7 +1085,7 @@ private:
         s.dt = dt_;
         s.delay = delay_;
         s.history = history_;
-        s.track_bits = has_synapses;
+        s.track_bits = has_synapses || (opt_.debug_checks && hist_);
         s.det_cnt = det_cnt_.get();
         s.det_off = det_off_.get();
         s.det_fill = det_fill_.get();
@@ -1239,15 +1298,54 @@ private:
     static constexpr int kUpdateBlock = 256;
     static constexpr int kReceiveBlock = 256;
     static constexpr uint32_t kGraphSteps = 16;
+    static constexpr int kWinBlock = 512;
+    static constexpr uint32_t kCompactTiles = 1024;  // k_update + k_compact up to this many tiles
+
+    // generic step: update -> [compact] -> catch-up -> receive.  Spike
+    // compaction (k_compact) is fused into the catch-up launch when the
+    // frame it writes is not the one the catch-up reads (delay >= 2), and the
+    // catch-up's ages advance at the start of the windowed receive
+    void enqueue_catchup(int mode, bool fuse_compact = false, bool ages_later = false) {
+        if constexpr (has_synapses) {
+            if (hist_words_ == 1) {
+                const uint64_t items = uint64_t(mode == 1 ? n_ : std::min<uint32_t>(n_, 4096)) *
+                                       ((graph_.deg_max + 1023) / 1024);
+                uint32_t g = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(items, uint64_t(sms_) * 16)));
+                if (fuse_compact) {
+                    g = std::max(g, ntiles_update_);
+                    dev::k_catchup1<Model, true><<<g, 256, 0, stream_>>>(model_, state(), mode);
+                } else {
+                    dev::k_catchup1<Model, false><<<g, 256, 0, stream_>>>(model_, state(), mode);
+                }
+                if (!ages_later)
+                    dev::k_catchup_ages<Model><<<std::max<uint32_t>(1, std::min<uint32_t>((n_ + 255) / 256, sms_)), 256, 0,
+                                                 stream_>>>(state(), mode);
+            } else {
+                const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_, uint32_t(sms_) * 8));
+                dev::k_catchup<Model><<<grid, 256, 0, stream_>>>(model_, state(), mode);
+            }
+        }
+    }
 
     void enqueue_generic_step() {
         auto st = state();
-        dev::k_update<Model, kUpdateBlock><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
-        if constexpr (has_synapses)
-            dev::k_catchup<Model><<<std::max<uint32_t>(1, std::min<uint32_t>(n_, uint32_t(sms_) * 8)), 256, 0, stream_>>>(
-                model_, st, 0);
+        const bool compact = ntiles_update_ <= kCompactTiles;
+        const bool win = win_on_ && (exact_ || !atomic_recv_);
+        const bool fuse = compact && has_synapses && hist_words_ == 1 && delay_ >= 2 && !opt_.debug_checks;
+        const bool ages_later = has_synapses && hist_words_ == 1 && win;
+        if (compact) {
+            dev::k_update<Model, kUpdateBlock, false><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
+            if (!fuse) dev::k_compact<Model, kUpdateBlock><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(st);
+        } else {
+            dev::k_update<Model, kUpdateBlock, true><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
+        }
+        if (opt_.debug_checks) dev::k_check_frame<Model><<<1, 1024, 0, stream_>>>(st);
+        enqueue_catchup(0, fuse, ages_later);
+        win_.ages = ages_later ? 1u : 0u;
         const int rgrid = 8 * sms_;
-        if (exact_) {
+        if (win) {
+            dev::k_recv_win<Model, kWinBlock><<<win_.C, kWinBlock, win_smem_, stream_>>>(model_, st, win_);
+        } else if (exact_) {
             dev::k_det_events<Model, kReceiveBlock, false><<<rgrid, kReceiveBlock, 0, stream_>>>(st);
             dev::k_det_scan<Model, 1024><<<1, 1024, 0, stream_>>>(st);
             dev::k_det_events<Model, kReceiveBlock, true><<<rgrid, kReceiveBlock, 0, stream_>>>(st);
@@ -1328,6 +1426,7 @@ private:
         kernel_seconds_ += ms * 1e-3;
         if (flags_host_[0]) throw device_error("spike log overflow (batch too large for the frame log)");
         if (flags_host_[1]) throw device_error("ordered delivery scratch overflow");
+        check_debug_flags();
 
         // per-step bookkeeping, frames_consumed (engine.hpp:371-380)
         for (uint32_t k = 0; k < b; ++k) {
@@ -1383,6 +1482,11 @@ private:
                                                   stream_));
             SYNQ_CUDA(cudaGetLastError());
             launches_ += 1;
+            if (opt_.debug_checks) {
+                dev::k_check_persist<Model><<<b, 256, 0, stream_>>>(ps, t0, b);
+                SYNQ_CUDA(cudaGetLastError());
+                launches_ += 1;
+            }
             SYNQ_CUDA(cudaEventRecord(fl.ev[1], stream_));
             uint32_t* hb = step_buf_.data() + size_t(slot) * 2 * batch_cap_;
             SYNQ_CUDA(cudaMemcpyAsync(hb, ps.step_spikes, sizeof(uint32_t) * 2 * b, cudaMemcpyDeviceToHost, stream_));
@@ -1418,7 +1522,12 @@ private:
     }
 
     uint64_t kernels_per_step() const {
-        return 2 + (has_synapses ? 1 : 0) + (exact_ ? 3 : 0);
+        const bool win = win_on_ && (exact_ || !atomic_recv_);
+        const bool compact = ntiles_update_ <= kCompactTiles;
+        const bool fuse = compact && has_synapses && hist_words_ == 1 && delay_ >= 2 && !opt_.debug_checks;
+        const bool ages_sep = has_synapses && hist_words_ == 1 && !win;
+        return 2 + (compact && !fuse ? 1 : 0) + (has_synapses ? 1 : 0) + (ages_sep ? 1 : 0) + (!win && exact_ ? 3 : 0) +
+               (opt_.debug_checks ? 1 : 0);
     }
 
     // frames logged_upto_ .. last are the next entries of `log`, in order.
@@ -1454,6 +1563,18 @@ private:
             d2h_bytes_ += 8 + 4 * logged;
             emit_logged(plog_[0].data(), logged, t_ - 1, plog_cnt_[0].data(), logged_upto_);
         }
+    }
+
+    // device-side check_frame results (k_check_frame / k_check_persist)
+    void check_debug_flags() {
+        if (!opt_.debug_checks || !flags_host_[3]) return;
+        const uint32_t f = flags_host_[3];
+        flags_host_[3] = 0;
+        const uint32_t zero = 0;
+        SYNQ_CUDA(cudaMemcpyAsync(flags_.get() + 3, &zero, sizeof zero, cudaMemcpyHostToDevice, stream_));
+        SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        if (f & 1) throw std::logic_error("spike frame not sorted/unique");
+        throw std::logic_error("spike queue and bitmask disagree");
     }
 
     void emit(int64_t t, std::span<const uint32_t> frame) {
@@ -1533,6 +1654,7 @@ private:
     dev_array<uint32_t> queue_, qcount_;
     uint32_t Q_ = 1;
     dev_array<unsigned long long> counters_dev_, tile_status_, log_cursor_;
+    dev_array<uint32_t> tile_bal_;
     dev_array<uint32_t> tile_ctr_, done_ctr_, flags_;
     uint32_t ntiles_update_ = 1;
     dev_array<int64_t> t_dev_, t0_dev_;
@@ -1577,6 +1699,10 @@ private:
     uint32_t bound_[dev::kMaxClasses] = {};
     float delta_[dev::kMaxClasses] = {};
     dev_array<float> fold_tab_;
+    dev::recv_win win_{};  // generic engine: ordered windowed receive
+    dev_array<uint32_t> win_lo_dev_, win_split_;
+    size_t win_smem_ = 0;
+    bool win_on_ = false, atomic_recv_ = false;
     uint32_t fold_t0_ = 0, fold_t1_ = 0;
     uint32_t win_cap_ = 0, pieces_ = 0, publishers_ = 0, stage_items_ = 0;
     dev_array<uint32_t> piece_src_;

@@ -29,4 +29,5 @@ def golden():
         "adj": np.load(os.path.join(d, "adjacency.npz")),
         "runs": np.load(os.path.join(d, "runs.npz")),
         "big": np.load(os.path.join(d, "big.npz")),
+        "bigp": np.load(os.path.join(d, "bigp.npz")) if os.path.exists(os.path.join(d, "bigp.npz")) else {},
     }

@@ -301,6 +301,46 @@ void test_reinit() {
     CHECK(net.persistent());
 }
 
+// debug_checks (engine.hpp:374-378, 440-446): the device-side frame checks
+// (sorted / unique, queue size == bitmask popcount, pieces inside their
+// ranges) run every step on both engines and pass on real runs; frames and
+// state are unchanged by them
+template <class M>
+void check_debug_run(model_build<M> b, int64_t steps, const char* name) {
+    engine_options opt;
+    opt.seed = 3;
+    opt.deterministic = true;
+    opt.debug_checks = true;
+    network<M> net(b.desc, b.model, opt);
+    frame_log log;
+    net.set_spike_tap(std::ref(log));
+    bool ok = true;
+    try {
+        net.run(steps);
+    } catch (const std::exception& e) {
+        std::printf("  %s: %s\n", name, e.what());
+        ok = false;
+    }
+    CHECK(ok);
+    opt.debug_checks = false;
+    network<M> ref(b.desc, b.model, opt);
+    frame_log rlog;
+    ref.set_spike_tap(std::ref(rlog));
+    ref.run(steps);
+    CHECK(log.frames == rlog.frames);
+    size_t spikes = 0;
+    for (const auto& f : log.frames) spikes += f.size();
+    CHECK(spikes > 0);
+    std::printf("  %s: %zu spikes, engine %s\n", name, spikes, net.persistent() ? "persistent" : "graph");
+}
+
+void test_debug_checks() {
+    std::printf("debug_checks\n");
+    check_debug_run(build_vogels(1000, builtin_defaults()), 600, "vogels");
+    check_debug_run(build_brunel_plus(400, builtin_defaults()), 300, "brunel+");
+    check_debug_run(build_pingpong(builtin_defaults()), 200, "pingpong");
+}
+
 // writes through a host span reach the device before the next step
 void test_span_writeback() {
     std::printf("span_writeback\n");
@@ -426,6 +466,7 @@ int main(int argc, char** argv) {
     run("reinit", test_reinit);
     run("span_writeback", test_span_writeback);
     run("accumulation_modes", test_accumulation_modes);
+    run("debug_checks", test_debug_checks);
     run("plan", test_plan);
     if (only == "plan_large") test_plan_large();
     if (only.empty() || only == "lazy") {

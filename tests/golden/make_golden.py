@@ -199,6 +199,48 @@ def big_vectors(workdir: str = "/tmp/synq_big"):
     return meta
 
 
+# Brunel+ (BASELINE.json configs[2]) at scale, short horizons: frames,
+# neuron state, ages and the synapse state after flush (sha256 per field)
+BIGP = [("brunel+", 100_000_000, 1, 400), ("brunel+", 1_000_000_000, 1, 100)]
+
+
+def bigp_vectors(workdir: str = "/tmp/synq_bigp"):
+    os.makedirs(workdir, exist_ok=True)
+    out, meta = {}, {}
+    for model, syn, seed, steps in BIGP:
+        tag = f"brunelp_{syn:.0e}_s{seed}_t{steps}".replace("+", "")
+        base = os.path.join(workdir, tag)
+        if not os.path.exists(base + ".counters"):
+            O.golden("big", model, syn, seed, steps, base)
+        hdr = np.fromfile(base + ".adj", np.uint32, count=4)
+        neurons, pitch, deg_max = int(hdr[0]), int(hdr[1]), int(hdr[2])
+        counts, ids = O.split_frames(np.fromfile(base + ".frames", np.uint32))
+        st = np.fromfile(base + ".state", np.uint32).reshape(3, neurons)
+        ages = np.fromfile(base + ".ages", np.uint32)
+        syn_sha = []
+        cap = neurons * deg_max
+        mm = np.memmap(base + ".syn", np.uint32, "r")
+        for f in range(3):
+            h = hashlib.sha256()
+            for a in range(f * cap, (f + 1) * cap, 1 << 26):
+                h.update(np.ascontiguousarray(mm[a:min((f + 1) * cap, a + (1 << 26))]).tobytes())
+            syn_sha.append(h.hexdigest())
+        counters = {}
+        for fn in (".counters", ".preflush"):
+            for line in open(base + fn):
+                k, v = line.strip().split("=")
+                counters[("preflush_" if fn == ".preflush" else "") + k] = int(v)
+        out[f"{tag}_counts"] = counts
+        out[f"{tag}_digests"] = frame_digests(counts, ids)
+        meta[tag] = {"model": model, "synapses": syn, "seed": seed, "steps": steps, "neurons": neurons,
+                     "deg_max": deg_max, "pitch": pitch,
+                     "state_sha256": [hashlib.sha256(st[i].tobytes()).hexdigest() for i in range(3)],
+                     "ages_sha256": hashlib.sha256(ages.tobytes()).hexdigest(), "syn_sha256": syn_sha,
+                     "counters": counters}
+    np.savez_compressed(os.path.join(HERE, "bigp.npz"), **out)
+    return meta
+
+
 # synthetic sweep (BASELINE.json configs[3]) at a reduced budget: every
 # (p, rate) point of the bench grid, S = 1e6 synapses, seed 1, 2000 steps
 SWEEP_S, SWEEP_STEPS = 1_000_000, 2000
@@ -233,11 +275,13 @@ def sweep_vectors():
 def main():
     if not O.have_reference():
         raise SystemExit("oracle/_ref not built (needs /root/reference): make -C oracle")
-    if sys.argv[1:] and sys.argv[1] in ("big", "sweep"):
+    if sys.argv[1:] and sys.argv[1] in ("big", "sweep", "bigp"):
         path = os.path.join(HERE, "golden.json")
         meta = json.load(open(path))
         if sys.argv[1] == "big":
             meta["big"] = big_vectors()
+        elif sys.argv[1] == "bigp":
+            meta["bigp"] = bigp_vectors()
         else:
             meta["sweep"] = sweep_vectors()
         with open(path, "w") as fh:
@@ -247,7 +291,7 @@ def main():
     rng_vectors()
     plan_vectors()
     meta = {"adjacency": adj_vectors(), "runs": run_vectors(), "big": big_vectors(),
-            "sweep": sweep_vectors()}
+            "sweep": sweep_vectors(), "bigp": bigp_vectors()}
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
     print("golden fixtures written to", HERE)

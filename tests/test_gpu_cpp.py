@@ -12,7 +12,7 @@ BIN = os.path.join(ROOT, "build", "test_network")
 pytestmark = pytest.mark.gpu
 
 CASES = ["delay_property", "pingpong_flag_reference", "silent_expiry", "ages_bound", "reinit",
-         "span_writeback", "accumulation_modes", "lazy", "plan", "plan_large"]
+         "span_writeback", "accumulation_modes", "debug_checks", "lazy", "plan", "plan_large"]
 
 
 @pytest.mark.parametrize("case", CASES)

@@ -85,3 +85,38 @@ def test_brunel_1e9_full_second_bit_exact(golden, big_sim):
     assert c["spikes"] == rc["spikes"]
     assert c["deliveries"] == rc["deliveries"]
     assert c["frames_consumed"] == rc["frames_consumed"]
+
+
+# ---- Brunel+ (BASELINE.json configs[2]) at 1e8 and 1e9 synapses, short
+# horizons (tests/golden/make_golden.py bigp): frames, neuron state, ages,
+# then the synapse state after flush (sha256 per field), ordered mode.
+@pytest.mark.parametrize("tag", ["brunelp_1e08_s1_t400", "brunelp_1e09_s1_t100"])
+def test_brunel_plus_at_scale_bit_exact(golden, tag):
+    if "bigp" not in golden["meta"] or tag not in golden["meta"]["bigp"]:
+        pytest.skip("bigp goldens not generated")
+    m = golden["meta"]["bigp"][tag]
+    big = golden["bigp"]
+    sim = synq.Sim("brunel+", opts=synq.Opts(seed=m["seed"], deterministic=True, record=True),
+                   synapses=m["synapses"])
+    assert sim.neurons == m["neurons"] and sim.exact
+    sim.run(m["steps"])
+    counts, ids = sim.frames()
+    diff = np.nonzero(counts != big[f"{tag}_counts"])[0]
+    assert len(diff) == 0, f"spike counts first differ at step {diff[0]}"
+    diff = np.nonzero(digests(counts, ids) != big[f"{tag}_digests"])[0]
+    assert len(diff) == 0, f"spike ids first differ at step {diff[0]}"
+    for i in range(3):
+        f = sim.neuron_field(i).view(np.uint32)
+        assert hashlib.sha256(f.tobytes()).hexdigest() == m["state_sha256"][i], i
+    assert hashlib.sha256(sim.ages().tobytes()).hexdigest() == m["ages_sha256"]
+    c, rc = sim.counters(), m["counters"]
+    assert c["synapse_updates"] == rc["preflush_synapse_updates"]
+    sim.flush()
+    for i in range(3):
+        f = sim.synapse_field(i).view(np.uint32)
+        assert hashlib.sha256(f.tobytes()).hexdigest() == m["syn_sha256"][i], i
+        del f
+    c = sim.counters()
+    assert c["spikes"] == rc["spikes"] and c["deliveries"] == rc["deliveries"]
+    assert c["synapse_updates"] == rc["synapse_updates"]
+    sim.close()

@@ -18,6 +18,7 @@ print(f"{model} syn={sim.synapses} n={sim.neurons} steps={steps} spikes={c['spik
 if prof:
     pc = sim.phase_cycles()
     print('update detail (pacing):', pc.get('update_detail'))
+    print('pipeline slots (cycles/step; passes per step):', pc.get('pipeline'))
     for key in ('mean', 'pacing'):
         tot = sum(pc[key].values())
         print(f'phase cycles/step ({key}, {pc["tiles"]} CTAs):', pc[key], 'total', round(tot),
