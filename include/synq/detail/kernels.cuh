@@ -51,6 +51,13 @@ constexpr bool model_uses_rng() {
         return false;
 }
 
+template <class M>
+constexpr bool model_has_plastic() {
+    return requires(const M& m, uint32_t a, uint32_t b) { { m.plastic(a, b) } -> std::convertible_to<bool>; };
+}
+// a model exposing plastic(src, dst) declares update_synapse a no-op for the
+// other synapses (benchmarks.hpp brunel_plus_model): catch-up skips them
+
 enum counter_slot : int { C_SPIKES = 0, C_DELIVERIES = 1, C_SYN_UPDATES = 2, C_EXPIRY = 3, C_COUNT = 8 };
 
 template <class M>
@@ -74,6 +81,8 @@ struct engine_state {
     uint32_t* ages;
     uint32_t* expiring;
     uint32_t* expiring_count;
+    uint8_t* caught;              // k_catchup1 (mode 0): ages advance to t + 1 in the next k_update
+    const uint8_t* row_plastic;   // models with plastic(): row holds a plastic synapse (else nullptr)
 
     unsigned long long* counters;
     unsigned long long* tile_status;  // decoupled look-back, one word per id tile
@@ -222,9 +231,15 @@ __global__ void k_init_synapses(M model, engine_state<M> st) {
     for (uint32_t s = warp; s < st.n; s += nwarps) {
         const uint32_t d = st.degree[s];
         const uint32_t* row = st.cells + static_cast<uint64_t>(s) * st.pitch;
+        bool any = false;
         for (uint32_t k = lane; k < d; k += 32) {
             global_synapse<SF> syn{static_cast<uint64_t>(s) * st.deg_max + k, s, row[k], st.sf};
             model.init_synapse(syn);
+            if constexpr (model_has_plastic<M>()) any |= model.plastic(s, row[k]);
+        }
+        if constexpr (model_has_plastic<M>()) {
+            any = __any_sync(0xffffffffu, any);
+            if (lane == 0 && st.row_plastic) const_cast<uint8_t*>(st.row_plastic)[s] = any ? 1 : 0;
         }
     }
 }
@@ -272,6 +287,10 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
             *w = (*w & ~(1ull << (slot & 63))) | (static_cast<uint64_t>(spk) << (slot & 63));
         }
         if constexpr (kSyn) {  // engine.hpp:318-330
+            if (st.caught && st.caught[i]) {  // caught up through t - 1 by the last step's k_catchup1
+                st.caught[i] = 0;
+                st.ages[i] = static_cast<uint32_t>(t);
+            }
             const bool transmits = (st.delay == 1) ? spk : hist_bit(st, i, t - st.delay + 1);
             if (!transmits && static_cast<int64_t>(st.ages[i]) + st.history <= t + st.delay + 1) {
                 const uint32_t slot = atomicAdd(st.expiring_count, 1u);
@@ -507,10 +526,6 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
 // plastic(src, dst) declares update_synapse a no-op for the other synapses
 // (benchmarks.hpp brunel_plus_model), which are skipped.  Same results as
 // k_catchup, bit for bit.
-template <class M>
-constexpr bool model_has_plastic() {
-    return requires(const M& m, uint32_t a, uint32_t b) { { m.plastic(a, b) } -> std::convertible_to<bool>; };
-}
 SYNQ_DEV uint64_t rotr64(uint64_t x, uint32_t r) { return r ? (x >> r) | (x << (64 - r)) : x; }
 
 // the catch-up list of step t: frame(due) U expiring (mode 0), or every
@@ -582,14 +597,21 @@ __global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st
     const uint32_t mc = (st.deg_max + U * 256 - 1) / (U * 256);
     const uint64_t items = static_cast<uint64_t>(cl.total) * mc;
     for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const uint32_t kq = static_cast<uint32_t>(it / mc), ch = static_cast<uint32_t>(it % mc);
+        const uint32_t kq = static_cast<uint32_t>(it / mc), ch = static_cast<uint32_t>(it - uint64_t(kq) * mc);
         const uint32_t nid = cl.at(st, mode, kq);
+        // a row without a plastic synapse: every update_synapse is a no-op,
+        // only its counter and age move (chunk 0, one thread)
+        const bool plastic_row = !st.row_plastic || st.row_plastic[nid];
+        if (!plastic_row && (ch != 0 || threadIdx.x != 0)) continue;
         const int64_t a0 = st.ages[nid];
         if (a0 > through) continue;
         const uint32_t n = static_cast<uint32_t>(through - a0 + 1);  // <= 64 under the expiry rule
         const uint32_t d = st.degree[nid];
-        if (ch == 0 && threadIdx.x == 0)
+        if (ch == 0 && threadIdx.x == 0) {
             atomicAdd(&st.counters[C_SYN_UPDATES], static_cast<unsigned long long>(d) * n);
+            if (mode == 0) st.caught[nid] = 1;
+        }
+        if (!plastic_row) continue;
         const uint32_t k0 = ch * U * 256 + threadIdx.x;
         if (k0 >= d) continue;
         const uint64_t lastn = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
@@ -644,6 +666,18 @@ __global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st
             store_syn_changed(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 256, sv[u], s0);
         }
     }
+}
+
+// pending k_catchup1 ages (caught flags) applied outside a step: before a
+// flush and when run() returns (host reads of ages)
+template <class M>
+__global__ void k_apply_caught(engine_state<M> st) {
+    const int64_t t = *st.t_dev;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < st.n; i += gridDim.x * blockDim.x)
+        if (st.caught[i]) {
+            st.caught[i] = 0;
+            st.ages[i] = static_cast<uint32_t>(t);
+        }
 }
 
 template <class M>
@@ -721,7 +755,7 @@ struct recv_win {
     uint32_t ecap;  // events staged per chunk
     uint32_t ages;  // advance the ages of the step's k_catchup1 list first
 };
-constexpr int kWinTPT = 4;      // targets per thread
+constexpr int kWinTPT = 2;      // targets per thread (1024-thread CTAs)
 constexpr int kWinSpikes = 256;  // spikes per chunk (8 mask words per target)
 
 // synapse handle on the staged copy of an event's synapse state
@@ -744,13 +778,17 @@ struct staged_synapse {
             return staged_offset<I - 1>(ecap) + ((sizeof(field_t<I - 1, FieldList>) * ecap + 15) & ~size_t(15));
     }
 };
+// stage synapse i's fields at e (working copy) and e + half (original)
 template <class FieldList, size_t I = 0>
-SYNQ_DEV void stage_syn(const field_ptrs<FieldList>& f, uint64_t i, unsigned char* base, uint32_t ecap, uint32_t e) {
+SYNQ_DEV void stage_syn(const field_ptrs<FieldList>& f, uint64_t i, unsigned char* base, uint32_t ecap2, uint32_t e,
+                        uint32_t half) {
     if constexpr (I < FieldList::count) {
         using T = field_t<I, FieldList>;
-        reinterpret_cast<T*>(base + staged_synapse<FieldList>::template staged_offset<I>(ecap))[e] =
-            f.template get<I>()[i];
-        stage_syn<FieldList, I + 1>(f, i, base, ecap, e);
+        T* a = reinterpret_cast<T*>(base + staged_synapse<FieldList>::template staged_offset<I>(ecap2));
+        const T x = f.template get<I>()[i];
+        a[e] = x;
+        a[e + half] = x;
+        stage_syn<FieldList, I + 1>(f, i, base, ecap2, e, half);
     }
 }
 // staged arrays hold 2 x half entries per field: [0, half) working copies,
@@ -763,15 +801,6 @@ SYNQ_DEV void unstage_syn(const field_ptrs<FieldList>& f, uint64_t i, const unsi
         const T* a = reinterpret_cast<const T*>(base + staged_synapse<FieldList>::template staged_offset<I>(ecap2));
         if (!same_bits(a[e], a[e + half])) f.template get<I>()[i] = a[e];
         unstage_syn<FieldList, I + 1>(f, i, base, ecap2, e, half);
-    }
-}
-template <class FieldList, size_t I = 0>
-SYNQ_DEV void copy_staged(unsigned char* base, uint32_t ecap2, uint32_t n) {
-    if constexpr (I < FieldList::count) {
-        using T = field_t<I, FieldList>;
-        T* a = reinterpret_cast<T*>(base + staged_synapse<FieldList>::template staged_offset<I>(ecap2));
-        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) a[e + ecap2 / 2] = a[e];
-        copy_staged<FieldList, I + 1>(base, ecap2, n);
     }
 }
 
@@ -798,12 +827,7 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
     const int64_t due = t - static_cast<int64_t>(st.delay) + 1;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t c = blockIdx.x, C = rw.C;
-    if constexpr (kSyn)
-        if (rw.ages) {
-            catchup_list<M> cl;
-            cl.load(st, 0, t);
-            advance_ages(st, cl, 0);
-        }
+
     const uint32_t lo = rw.lo[c], wn = rw.lo[c + 1] - lo;
     unsigned long long mine = 0;
     if (due >= 0 && wn > 0) {
@@ -883,7 +907,8 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
                         ek[u] = s_sb[a] + (e - s_off[a]);
                         tg[u] = st.cells[static_cast<uint64_t>(s_spk[a]) * st.pitch + ek[u]];
                         if constexpr (kSyn)
-                            stage_syn(st.sf, static_cast<uint64_t>(s_spk[a]) * st.deg_max + ek[u], s_syn, 2 * ecap, e);
+                            stage_syn(st.sf, static_cast<uint64_t>(s_spk[a]) * st.deg_max + ek[u], s_syn, 2 * ecap, e,
+                                      ecap);
                     }
                 }
 #pragma unroll
@@ -898,9 +923,6 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
                     }
                 }
             }
-            __syncthreads();
-            if constexpr (kSyn)  // original copy for the write-back comparison
-                copy_staged<SF>(s_syn, 2 * ecap, E);
             __syncthreads();
             // (3) target offsets (exclusive scan over the window)
             uint32_t carry = 0;

@@ -252,6 +252,7 @@ public:
         if constexpr (has_synapses) {
             t0 = clock::now();
             ages_.zero(stream_);
+            caught_.zero(stream_);
             for (auto& col : syn_cols_) col.zero(stream_);
             if (graph_.edges)
                 dev::k_init_synapses<Model><<<grid_for(uint64_t(n_) * 32, 256), 256, 0, stream_>>>(model_, state());
@@ -324,6 +325,13 @@ public:
                 run_batch(static_cast<uint32_t>(b));
                 steps -= b;
             }
+            if constexpr (has_synapses)  // the last step's catch-up ages (k_catchup1 leaves them to k_update)
+                if (caught_) {
+                    dev::k_apply_caught<Model><<<std::max<uint32_t>(1, std::min<uint32_t>((n_ + 255) / 256, sms_)), 256, 0,
+                                                 stream_>>>(state());
+                    SYNQ_CUDA(cudaGetLastError());
+                    launches_ += 1;
+                }
         }
         SYNQ_CUDA(cudaEventRecord(ev_[1], stream_));
         SYNQ_CUDA(cudaEventSynchronize(ev_[1]));
@@ -600,6 +608,8 @@ private:
             detail::alloc_fields<synapse_fields>(syn_cols_, sptrs_, cap, stream_);
             host_synapses_.resize(cap);
             ages_.resize(std::max<uint32_t>(1, n_));
+            caught_.resize(std::max<uint32_t>(1, n_));
+            if constexpr (dev::model_has_plastic<Model>()) row_plastic_.resize(std::max<uint32_t>(1, n_));
             expiring_.resize(std::max<uint32_t>(1, n_));
             expiring_count_.resize(1);
             hist_words_ = (history_ + 63) / 64;
@@ -1064,6 +1074,8 @@ private:
         s.hist = hist_.get();
         s.hist_words = hist_words_;
         s.ages = ages_.get();
+        s.caught = caught_ ? caught_.get() : nullptr;
+        s.row_plastic = row_plastic_ ? row_plastic_.get() : nullptr;
         s.expiring = expiring_.get();
         s.expiring_count = expiring_count_.get();
         s.counters = counters_dev_.get();
@@ -1298,14 +1310,14 @@ private:
     static constexpr int kUpdateBlock = 256;
     static constexpr int kReceiveBlock = 256;
     static constexpr uint32_t kGraphSteps = 16;
-    static constexpr int kWinBlock = 512;
+    static constexpr int kWinBlock = 1024;
     static constexpr uint32_t kCompactTiles = 1024;  // k_update + k_compact up to this many tiles
 
     // generic step: update -> [compact] -> catch-up -> receive.  Spike
     // compaction (k_compact) is fused into the catch-up launch when the
     // frame it writes is not the one the catch-up reads (delay >= 2), and the
     // catch-up's ages advance at the start of the windowed receive
-    void enqueue_catchup(int mode, bool fuse_compact = false, bool ages_later = false) {
+    void enqueue_catchup(int mode, bool fuse_compact = false) {
         if constexpr (has_synapses) {
             if (hist_words_ == 1) {
                 const uint64_t items = uint64_t(mode == 1 ? n_ : std::min<uint32_t>(n_, 4096)) *
@@ -1317,7 +1329,7 @@ private:
                 } else {
                     dev::k_catchup1<Model, false><<<g, 256, 0, stream_>>>(model_, state(), mode);
                 }
-                if (!ages_later)
+                if (mode == 1)  // (mode 0: the next k_update advances the caught neurons' ages)
                     dev::k_catchup_ages<Model><<<std::max<uint32_t>(1, std::min<uint32_t>((n_ + 255) / 256, sms_)), 256, 0,
                                                  stream_>>>(state(), mode);
             } else {
@@ -1332,7 +1344,6 @@ private:
         const bool compact = ntiles_update_ <= kCompactTiles;
         const bool win = win_on_ && (exact_ || !atomic_recv_);
         const bool fuse = compact && has_synapses && hist_words_ == 1 && delay_ >= 2 && !opt_.debug_checks;
-        const bool ages_later = has_synapses && hist_words_ == 1 && win;
         if (compact) {
             dev::k_update<Model, kUpdateBlock, false><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
             if (!fuse) dev::k_compact<Model, kUpdateBlock><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(st);
@@ -1340,8 +1351,7 @@ private:
             dev::k_update<Model, kUpdateBlock, true><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
         }
         if (opt_.debug_checks) dev::k_check_frame<Model><<<1, 1024, 0, stream_>>>(st);
-        enqueue_catchup(0, fuse, ages_later);
-        win_.ages = ages_later ? 1u : 0u;
+        enqueue_catchup(0, fuse);
         const int rgrid = 8 * sms_;
         if (win) {
             dev::k_recv_win<Model, kWinBlock><<<win_.C, kWinBlock, win_smem_, stream_>>>(model_, st, win_);
@@ -1525,8 +1535,7 @@ private:
         const bool win = win_on_ && (exact_ || !atomic_recv_);
         const bool compact = ntiles_update_ <= kCompactTiles;
         const bool fuse = compact && has_synapses && hist_words_ == 1 && delay_ >= 2 && !opt_.debug_checks;
-        const bool ages_sep = has_synapses && hist_words_ == 1 && !win;
-        return 2 + (compact && !fuse ? 1 : 0) + (has_synapses ? 1 : 0) + (ages_sep ? 1 : 0) + (!win && exact_ ? 3 : 0) +
+        return 2 + (compact && !fuse ? 1 : 0) + (has_synapses ? 1 : 0) + (!win && exact_ ? 3 : 0) +
                (opt_.debug_checks ? 1 : 0);
     }
 
@@ -1655,6 +1664,7 @@ private:
     uint32_t Q_ = 1;
     dev_array<unsigned long long> counters_dev_, tile_status_, log_cursor_;
     dev_array<uint32_t> tile_bal_;
+    dev_array<uint8_t> caught_, row_plastic_;
     dev_array<uint32_t> tile_ctr_, done_ctr_, flags_;
     uint32_t ntiles_update_ = 1;
     dev_array<int64_t> t_dev_, t0_dev_;

@@ -95,6 +95,7 @@ def lib() -> C.CDLL:
     sig("synq_sim_flush", st, vp)
     sig("synq_sim_neurons", u32, vp)
     sig("synq_sim_synapses", u64, vp)
+    sig("synq_sim_ages", st, vp, vp, u64)
     sig("synq_sim_synapse_capacity", u64, vp)
     sig("synq_sim_now", i64, vp)
     sig("synq_sim_dt", dbl, vp)
@@ -361,6 +362,11 @@ class Sim:
         out = np.empty(max(self.synapse_capacity, 1), dtype)
         check(lib().synq_sim_synapse_field(self.h, f, _p(out), out.nbytes))
         return out[: self.synapse_capacity]
+
+    def ages(self) -> np.ndarray:
+        out = np.empty(max(self.neurons, 1), np.uint32)
+        check(lib().synq_sim_ages(self.h, _p(out), len(out)))
+        return out[: self.neurons]
 
     def graph(self) -> np.ndarray:
         pitch, dmax = C.c_uint32(), C.c_uint32()

@@ -67,6 +67,7 @@ public:
     virtual const std::vector<uint32_t>& step_spikes() const = 0;
     virtual void neuron_field_bytes(uint32_t f, void* out, uint64_t bytes) = 0;
     virtual void synapse_field_bytes(uint32_t f, void* out, uint64_t bytes) = 0;
+    virtual void ages_copy(uint32_t* out, uint64_t capacity) = 0;
     virtual const adjacency_list& graph() const = 0;
     virtual uint64_t fixups() const = 0;
     virtual void device_time(double out[2]) const = 0;
@@ -204,6 +205,15 @@ public:
     const std::vector<uint32_t>& step_spikes() const override { return net_->step_spike_counts(); }
     void neuron_field_bytes(uint32_t f, void* out, uint64_t bytes) override {
         copy_neuron_field<typename M::neuron_fields>(*net_, f, out, bytes);
+    }
+    void ages_copy(uint32_t* out, uint64_t capacity) override {
+        if constexpr (network<M>::has_synapses) {
+            auto a = net_->ages();
+            if (capacity < a.size()) throw std::invalid_argument("buffer too small for ages");
+            std::memcpy(out, a.data(), a.size_bytes());
+        } else {
+            throw std::invalid_argument("model has no synapse state");
+        }
     }
     void synapse_field_bytes(uint32_t f, void* out, uint64_t bytes) override {
         if constexpr (network<M>::has_synapses)
@@ -840,6 +850,14 @@ synq_status synq_sim_synapse_field(synq_sim* s, uint32_t field, void* out, uint6
     SYNQ_CHECK_HANDLE(out);
     return guarded([&] {
         s->impl->synapse_field_bytes(field, out, bytes);
+        return SYNQ_OK;
+    });
+}
+synq_status synq_sim_ages(synq_sim* s, uint32_t* out, uint64_t capacity) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(out);
+    return guarded([&] {
+        s->impl->ages_copy(out, capacity);
         return SYNQ_OK;
     });
 }
