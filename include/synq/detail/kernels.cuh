@@ -292,9 +292,21 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
                 st.ages[i] = static_cast<uint32_t>(t);
             }
             const bool transmits = (st.delay == 1) ? spk : hist_bit(st, i, t - st.delay + 1);
-            if (!transmits && static_cast<int64_t>(st.ages[i]) + st.history <= t + st.delay + 1) {
-                const uint32_t slot = atomicAdd(st.expiring_count, 1u);
-                st.expiring[slot] = i;
+            const int64_t a = st.ages[i];
+            if (!transmits && a + st.history <= t + st.delay + 1) {
+                atomicAdd(&st.counters[C_EXPIRY], 1ull);  // expiry_batches (engine.hpp:349)
+                if (st.row_plastic && !st.row_plastic[i]) {
+                    // no plastic synapse in the row: the catch-up through t is
+                    // only its counter and age (no replay, not listed)
+                    if (a <= t) {
+                        atomicAdd(&st.counters[C_SYN_UPDATES],
+                                  static_cast<unsigned long long>(st.degree[i]) * static_cast<unsigned long long>(t - a + 1));
+                        st.ages[i] = static_cast<uint32_t>(t + 1);
+                    }
+                } else {
+                    const uint32_t slot = atomicAdd(st.expiring_count, 1u);
+                    st.expiring[slot] = i;
+                }
             }
         }
     }
@@ -458,9 +470,7 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
             frame = st.queue + static_cast<uint64_t>(due % st.Q) * st.n;
             ntr = st.qcount[due % st.Q];
         }
-        const uint32_t nex = *st.expiring_count;
-        total = ntr + nex;
-        if (blockIdx.x == 0 && threadIdx.x == 0 && nex) atomicAdd(&st.counters[C_EXPIRY], nex);
+        total = ntr + *st.expiring_count;  // (k_update counts the expiring neurons)
     } else {
         total = st.n;
     }
@@ -528,6 +538,12 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
 // k_catchup, bit for bit.
 SYNQ_DEV uint64_t rotr64(uint64_t x, uint32_t r) { return r ? (x >> r) | (x << (64 - r)) : x; }
 
+// programmatic dependent launch (PDL): the primary lets its dependent grid
+// be scheduled early; the dependent waits for the primary's memory before
+// touching its outputs (both are no-ops without the launch attribute)
+SYNQ_DEV void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+SYNQ_DEV void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // the catch-up list of step t: frame(due) U expiring (mode 0), or every
 // neuron (mode 1, flush through t - 1)
 template <class M>
@@ -586,33 +602,36 @@ template <class M, bool kCompact = false>
 __global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st, int mode) {
     using SF = typename synapse_fields_of<M>::type;
     constexpr int U = 4;  // synapses per thread, loads batched
+    grid_launch_dependents();  // k_recv_win may start its prologue on SMs this grid frees
     const int64_t t = *st.t_dev;
     if constexpr (kCompact) compact_tiles<M, 256>(st, t);
     catchup_list<M> cl;
-    cl.load(st, mode, t);
-    if (mode == 0 && blockIdx.x == 0 && threadIdx.x == 0 && cl.total > cl.ntr)
-        atomicAdd(&st.counters[C_EXPIRY], cl.total - cl.ntr);
+    cl.load(st, mode, t);  // (k_update counts the expiring neurons)
     const int64_t through = cl.through;
-    // work item = (neuron, chunk of U x 256 synapses); ages advance later
-    const uint32_t mc = (st.deg_max + U * 256 - 1) / (U * 256);
+    // work item = (neuron, chunk of U x 32 synapses), one per warp: many
+    // items' load chains in flight per SM; ages advance later
+    constexpr uint32_t CH = U * 32;
+    const uint32_t lane = lane_id();
+    const uint32_t mc = (st.deg_max + CH - 1) / CH;
     const uint64_t items = static_cast<uint64_t>(cl.total) * mc;
-    for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t it = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < items; it += wstride) {
         const uint32_t kq = static_cast<uint32_t>(it / mc), ch = static_cast<uint32_t>(it - uint64_t(kq) * mc);
         const uint32_t nid = cl.at(st, mode, kq);
         // a row without a plastic synapse: every update_synapse is a no-op,
-        // only its counter and age move (chunk 0, one thread)
+        // only its counter and age move (chunk 0, one lane)
         const bool plastic_row = !st.row_plastic || st.row_plastic[nid];
-        if (!plastic_row && (ch != 0 || threadIdx.x != 0)) continue;
+        if (!plastic_row && (ch != 0 || lane != 0)) continue;
         const int64_t a0 = st.ages[nid];
         if (a0 > through) continue;
         const uint32_t n = static_cast<uint32_t>(through - a0 + 1);  // <= 64 under the expiry rule
         const uint32_t d = st.degree[nid];
-        if (ch == 0 && threadIdx.x == 0) {
+        if (ch == 0 && lane == 0) {
             atomicAdd(&st.counters[C_SYN_UPDATES], static_cast<unsigned long long>(d) * n);
             if (mode == 0) st.caught[nid] = 1;
         }
         if (!plastic_row) continue;
-        const uint32_t k0 = ch * U * 256 + threadIdx.x;
+        const uint32_t k0 = ch * CH + lane;
         if (k0 >= d) continue;
         const uint64_t lastn = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
         // pre bits: u - delay for u in [a0, through]; u - delay < 0 is false
@@ -634,7 +653,7 @@ __global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st
         bool on[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint32_t kk = k0 + u * 256;
+            const uint32_t kk = k0 + u * 32;
             on[u] = kk < d;
             dst[u] = on[u] ? row[kk] : 0u;
         }
@@ -645,7 +664,7 @@ __global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st
             if constexpr (model_has_plastic<M>()) on[u] = on[u] && model.plastic(nid, dst[u]);
             postw[u] = 0;
             if (on[u]) {
-                load_syn(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 256, sv[u]);
+                load_syn(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 32, sv[u]);
                 postw[u] = st.hist[dst[u]];
             }
         }
@@ -663,7 +682,7 @@ __global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st
             } else {
                 replay_window(model, sv[u], prew, rotr64(postw[u], r0) & lastn, n, st.dt);
             }
-            store_syn_changed(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 256, sv[u], s0);
+            store_syn_changed(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 32, sv[u], s0);
         }
     }
 }
@@ -906,9 +925,19 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
                         ej[u] = a;
                         ek[u] = s_sb[a] + (e - s_off[a]);
                         tg[u] = st.cells[static_cast<uint64_t>(s_spk[a]) * st.pitch + ek[u]];
-                        if constexpr (kSyn)
-                            stage_syn(st.sf, static_cast<uint64_t>(s_spk[a]) * st.deg_max + ek[u], s_syn, 2 * ecap, e,
-                                      ecap);
+                    }
+                }
+                // the synapse state of the due spikes' rows is the catch-up's
+                // output: with programmatic dependent launch this kernel got
+                // here while k_catchup1 was still running
+                if constexpr (kSyn) {
+                    if (g0 == 0 && e0 == 0) grid_dependency_wait();
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t e = e0 + u * BLOCK + tid;
+                        if (e < E)
+                            stage_syn(st.sf, static_cast<uint64_t>(s_spk[ej[u]]) * st.deg_max + ek[u], s_syn, 2 * ecap,
+                                      e, ecap);
                     }
                 }
 #pragma unroll
@@ -999,6 +1028,7 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
         }
         if (tid == 0 && mine) atomicAdd(&st.counters[C_DELIVERIES], mine);
     }
+    grid_dependency_wait();  // the epilogue resets what the catch-up still reads (t, expiring count)
     step_epilogue(st, t);
 }
 

@@ -674,6 +674,7 @@ private:
     void setup_recv_win() {
         if (const char* e = std::getenv("SYNQ_WINRECV"); e && std::atoi(e) == 0) return;
         if (const char* e = std::getenv("SYNQ_ATOMIC_RECV")) atomic_recv_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SYNQ_PDL")) pdl_ = std::atoi(e) != 0;
         if (n_ == 0 || graph_.edges == 0 || graph_.deg_max >= (1u << 24) || !graph_.cells) return;
         const uint32_t cap_t = uint32_t(dev::kWinTPT) * kWinBlock;
         const std::vector<uint32_t> indeg = in_degrees(graph_, stream_);
@@ -1320,9 +1321,8 @@ private:
     void enqueue_catchup(int mode, bool fuse_compact = false) {
         if constexpr (has_synapses) {
             if (hist_words_ == 1) {
-                const uint64_t items = uint64_t(mode == 1 ? n_ : std::min<uint32_t>(n_, 4096)) *
-                                       ((graph_.deg_max + 1023) / 1024);
-                uint32_t g = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(items, uint64_t(sms_) * 16)));
+                // warp items; 4 CTAs of 8 warps per SM (60 registers)
+                uint32_t g = static_cast<uint32_t>(sms_) * 4;
                 if (fuse_compact) {
                     g = std::max(g, ntiles_update_);
                     dev::k_catchup1<Model, true><<<g, 256, 0, stream_>>>(model_, state(), mode);
@@ -1354,7 +1354,22 @@ private:
         enqueue_catchup(0, fuse);
         const int rgrid = 8 * sms_;
         if (win) {
-            dev::k_recv_win<Model, kWinBlock><<<win_.C, kWinBlock, win_smem_, stream_>>>(model_, st, win_);
+            // programmatic dependent launch after k_catchup1 (its frame is an
+            // older step's when delay >= 2): the window prologue overlaps
+            // the catch-up's tail; SYNQ_PDL=0 launches it plainly
+            const bool pdl = has_synapses && hist_words_ == 1 && delay_ >= 2 && pdl_;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(win_.C);
+            cfg.blockDim = dim3(kWinBlock);
+            cfg.dynamicSmemBytes = win_smem_;
+            cfg.stream = stream_;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = pdl ? 1 : 0;
+            Model m = model_;
+            SYNQ_CUDA(cudaLaunchKernelEx(&cfg, dev::k_recv_win<Model, kWinBlock>, m, st, win_));
         } else if (exact_) {
             dev::k_det_events<Model, kReceiveBlock, false><<<rgrid, kReceiveBlock, 0, stream_>>>(st);
             dev::k_det_scan<Model, 1024><<<1, 1024, 0, stream_>>>(st);
@@ -1712,7 +1727,7 @@ private:
     dev::recv_win win_{};  // generic engine: ordered windowed receive
     dev_array<uint32_t> win_lo_dev_, win_split_;
     size_t win_smem_ = 0;
-    bool win_on_ = false, atomic_recv_ = false;
+    bool win_on_ = false, atomic_recv_ = false, pdl_ = true;
     uint32_t fold_t0_ = 0, fold_t1_ = 0;
     uint32_t win_cap_ = 0, pieces_ = 0, publishers_ = 0, stage_items_ = 0;
     dev_array<uint32_t> piece_src_;

@@ -1,0 +1,4 @@
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_cpp.py tests/test_gpu_rates.py tests/test_gpu_parity_big.py -q -p no:cacheprovider -k "not brunel_1e9" 2>&1 | grep -v "^$" | tail -30 > gpurun_out/r2r_test.txt
+timeout 300 python tools/plus_run.py 1e8 2000 > gpurun_out/r2r_plus.txt 2>&1
+timeout 300 python tools/plus_run.py 1e9 300 >> gpurun_out/r2r_plus.txt 2>&1
+timeout 600 ncu --graph-profiling node --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2r_plus_launches.csv python tools/plus_run.py 1e8 300 >> gpurun_out/r2r_plus.txt 2>&1
