@@ -620,25 +620,38 @@ __global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st
         const uint32_t nid = cl.at(st, mode, kq);
         // a row without a plastic synapse: every update_synapse is a no-op,
         // only its counter and age move (chunk 0, one lane)
+        // one round of independent loads per item: row flags, age, degree,
+        // history word, the chunk's row targets (the padded row is readable up
+        // to the pitch) and synapse state (up to deg_max); then the targets'
+        // history words
+        const uint32_t k0 = ch * CH + lane;
+        const uint32_t* row = st.cells + static_cast<uint64_t>(nid) * st.pitch;
         const bool plastic_row = !st.row_plastic || st.row_plastic[nid];
-        if (!plastic_row && (ch != 0 || lane != 0)) continue;
         const int64_t a0 = st.ages[nid];
+        const uint32_t d = st.degree[nid];
+        const uint64_t hw = st.hist[nid];
+        uint32_t dst[U];
+        synapse_state<SF> sv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t kk = k0 + u * 32;
+            dst[u] = kk < st.pitch ? row[kk] : 0xffffffffu;
+            if (kk < st.deg_max) load_syn(st.sf, static_cast<uint64_t>(nid) * st.deg_max + kk, sv[u]);
+        }
+        if (!plastic_row && (ch != 0 || lane != 0)) continue;
         if (a0 > through) continue;
         const uint32_t n = static_cast<uint32_t>(through - a0 + 1);  // <= 64 under the expiry rule
-        const uint32_t d = st.degree[nid];
         if (ch == 0 && lane == 0) {
             atomicAdd(&st.counters[C_SYN_UPDATES], static_cast<unsigned long long>(d) * n);
             if (mode == 0) st.caught[nid] = 1;
         }
         if (!plastic_row) continue;
-        const uint32_t k0 = ch * CH + lane;
         if (k0 >= d) continue;
         const uint64_t lastn = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
         // pre bits: u - delay for u in [a0, through]; u - delay < 0 is false
         const int64_t p0 = a0 - static_cast<int64_t>(st.delay);
         uint64_t prew = 0;
         if (n <= 64 && p0 + static_cast<int64_t>(n) > 0) {
-            const uint64_t hw = st.hist[nid];
             if (p0 >= 0) {
                 prew = rotr64(hw, static_cast<uint32_t>(p0 % 64));
             } else {
@@ -648,25 +661,13 @@ __global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st
         }
         prew &= lastn;
         const uint32_t r0 = static_cast<uint32_t>(a0 % 64);
-        const uint32_t* row = st.cells + static_cast<uint64_t>(nid) * st.pitch;
-        uint32_t dst[U];
         bool on[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t kk = k0 + u * 32;
-            on[u] = kk < d;
-            dst[u] = on[u] ? row[kk] : 0u;
-        }
-        synapse_state<SF> sv[U];
         uint64_t postw[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            on[u] = k0 + u * 32 < d;
             if constexpr (model_has_plastic<M>()) on[u] = on[u] && model.plastic(nid, dst[u]);
-            postw[u] = 0;
-            if (on[u]) {
-                load_syn(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 32, sv[u]);
-                postw[u] = st.hist[dst[u]];
-            }
+            postw[u] = on[u] ? st.hist[dst[u]] : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
