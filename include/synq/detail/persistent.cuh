@@ -60,6 +60,7 @@ struct persist_state {
     field_ptrs<NF> nf;
     xorshift* rng;
     const uint32_t* cells;
+    const uint32_t* degree;     // [n] out-degrees (k_solo)
     const uint32_t* split;      // [n][C+1]: receive-window boundaries of the CTAs
     const uint32_t* piece_lo;   // [P+1] piece boundaries in id order
     const uint32_t* cta_piece;  // [2C]: (A piece, B piece) of every local CTA

@@ -49,6 +49,7 @@
 #include "synq/detail/kernels.cuh"
 #include "synq/detail/persistent.cuh"
 #include "synq/detail/pipeline.cuh"
+#include "synq/detail/solo.cuh"
 #include "synq/detail/exchange.hpp"
 #include "synq/models/benchmarks.hpp"
 #include "synq/network_desc.hpp"
@@ -387,6 +388,7 @@ public:
     unsigned worker_count() const { return persistent_ ? tiles_ : static_cast<unsigned>(sms_); }
     bool persistent() const { return persistent_; }
     bool pipelined() const { return persistent_ && pipe_; }
+    bool solo() const { return persistent_ && solo_; }
     bool bitmap_delivery() const { return persistent_ && pipe_ && pipe_bm_; }
     bool exact() const { return exact_ || persistent_ || (win_on_ && !atomic_recv_); }
     uint64_t construction_fixups() const { return graph_.tie_fixups; }
@@ -819,10 +821,19 @@ private:
             const int64_t want = std::max<int64_t>((n + kNeuronsPerTile - 1) / kNeuronsPerTile, std::min<int64_t>(32, n / 32));
             return static_cast<uint32_t>(std::clamp<int64_t>(want, 1, sms_));
         };
-        uint32_t C = opt_.tiles ? opt_.tiles : tiles_for(n_);
+        // SYNQ_SOLO=1: the single-CTA engine (detail/solo.cuh) for networks
+        // of <= 4096 neurons.  Opt-in: measured 2.9-5x slower than the
+        // multi-CTA pipeline from 1,414 to 4,000 Vogels neurons (one SM
+        // issues the whole update)
+        bool solo = W == 1 && !opt_.shard_nccl && n_ <= dev::kSoloMaxNeurons && delay_ <= dev::kSoloMaxDelay &&
+                    (opt_.tiles == 0 || opt_.tiles == 1) && opt_.pipeline < 0 && !std::getenv("SYNQ_PIPELINE");
+        const char* solo_env = std::getenv("SYNQ_SOLO");
+        solo = solo && solo_env && std::atoi(solo_env) != 0;
+        uint32_t C = solo ? 1u : (opt_.tiles ? opt_.tiles : tiles_for(n_));
         C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), n_});
         const uint32_t max_local = 4 * NTH;  // register-resident state: <= 4 neurons per thread
-        if (uint64_t(C) * max_local < n_) C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (n_ + max_local - 1) / max_local));
+        if (!solo && uint64_t(C) * max_local < n_)
+            C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (n_ + max_local - 1) / max_local));
         // shards: contiguous rank ranges of the receiving region (by receive
         // cost) and of the update-only region (by count); then this rank's
         // range into C local pieces of each kind
@@ -882,7 +893,16 @@ private:
         SYNQ_CUDA(cudaGetDevice(&dev));
         SYNQ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         size_t smem = 0;
-        if (!setup_pipeline(K, wcap, longest, delay_, size_t(max_smem), smem, alo)) {
+        solo_ = false;
+        if (solo) {
+            if (C != 1) throw device_error("internal: single-CTA engine with several pieces");
+            smem = dev::solo_smem_bytes(uint32_t(K), wcap, n_);
+            if (smem + 16 * 1024 > size_t(max_smem) || longest > dev::kSoloMaxNeurons) return;
+            solo_ = true;
+            pipe_ = false;
+            pipe_bm_ = false;
+            npt_ = longest <= 1024 ? 1 : (longest <= 2048 ? 2 : 4);
+        } else if (!setup_pipeline(K, wcap, longest, delay_, size_t(max_smem), smem, alo)) {
             if (longest > max_local) return;
             // dynamic smem: counts only (delivery items are static)
             const size_t static_smem = 3 * (dev::kMaxPieces + 1) * 4 + 8192;
@@ -1236,9 +1256,16 @@ private:
         }
     }
 
-    uint32_t kernel_threads() const { return pipe_ ? pipe_threads_ : static_cast<uint32_t>(dev::kPersistThreads); }
+    uint32_t kernel_threads() const {
+        if (solo_) return static_cast<uint32_t>(dev::kSoloThreads);
+        return pipe_ ? pipe_threads_ : static_cast<uint32_t>(dev::kPersistThreads);
+    }
 
     const void* kernel_fn() const requires population_model {
+        if (solo_)
+            return npt_ == 1 ? reinterpret_cast<const void*>(dev::k_solo<Model, 1>)
+                             : (npt_ == 2 ? reinterpret_cast<const void*>(dev::k_solo<Model, 2>)
+                                          : reinterpret_cast<const void*>(dev::k_solo<Model, 4>));
         if (pipe_) return pipe_bm_ ? pipeline_fn<true>(pipe_uw_, pipe_npt_) : pipeline_fn<false>(pipe_uw_, pipe_npt_);
         return persistent_fn();
     }
@@ -1256,6 +1283,7 @@ private:
         p.nf = nptrs_;
         p.rng = rng_.get();
         p.cells = graph_.cells.get();
+        p.degree = graph_.degree.get();
         p.split = split_.get();
         p.piece_lo = tile_lo_.get();
         p.cta_piece = win_lo_.get();
@@ -1748,6 +1776,7 @@ private:
     int npt_select_ = 1;
     bool pipe_ = false;  // pipelined kernel (detail/pipeline.cuh)
     bool pipe_bm_ = false;  // ... with bitmap delivery
+    bool solo_ = false;     // single-CTA engine (detail/solo.cuh)
     dev_array<uint4> bm_;
     uint32_t bm_wq_ = 0, bm_row4_ = 0;
     uint32_t pipe_uw_ = 4, pipe_npt_ = 1, ring_R_ = 0, lead_ = 0, lag_ = 0, pf_cap_ = 0;

@@ -292,7 +292,8 @@ class Sim:
 
     @property
     def engine(self) -> str:
-        return {0: "graph", 1: "persistent", 2: "pipelined", 3: "pipelined-bitmap"}[lib().synq_sim_engine(self.h)]
+        return {0: "graph", 1: "persistent", 2: "pipelined", 3: "pipelined-bitmap", 4: "solo"}[
+            lib().synq_sim_engine(self.h)]
 
     @property
     def exact(self) -> bool:

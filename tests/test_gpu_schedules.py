@@ -25,7 +25,7 @@ pytestmark = pytest.mark.gpu
 
 
 def build(m, env, monkeypatch, **kw):
-    for k in ("SYNQ_BITMAP", "SYNQ_UW", "SYNQ_LAG", "SYNQ_LEAD", "SYNQ_PREFETCH", "SYNQ_STREAM", "SYNQ_WORKQ"):
+    for k in ("SYNQ_BITMAP", "SYNQ_UW", "SYNQ_LAG", "SYNQ_LEAD", "SYNQ_PREFETCH", "SYNQ_STREAM", "SYNQ_WORKQ", "SYNQ_SOLO"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, str(v))
@@ -141,5 +141,35 @@ def test_workqueue_delivery(golden, monkeypatch, tag, uw):
     sim = build(golden["meta"]["runs"][tag], {"SYNQ_WORKQ": 1, "SYNQ_BITMAP": 2, "SYNQ_UW": uw}, monkeypatch,
                 pipeline=1)
     assert sim.engine == "pipelined-bitmap"
+    check(sim, golden, tag)
+    sim.close()
+
+
+@pytest.mark.parametrize("tag", ["brunel_2000_s99_t3000_h0_d0", "vogels_1000_s99_t3000_h0_d0",
+                                 "vogels_500_s3_t500_h0_d3", "vogels_4000_s1_t10000_h0_d0"])
+@pytest.mark.parametrize("chunks", [None, "uneven"])
+def test_solo_engine_bit_exact(golden, monkeypatch, tag, chunks):
+    """Single-CTA engine (detail/solo.cuh, SYNQ_SOLO=1, <= 4096 neurons):
+    bit-exact, also when run() is cut into launches of odd sizes (the frames
+    of an earlier launch are delivered from global memory)."""
+    m = golden["meta"]["runs"][tag]
+    sim = build(m, {"SYNQ_SOLO": 1}, monkeypatch)
+    assert sim.engine == "solo", sim.engine
+    cuts = None
+    if chunks:
+        left, cuts = m["steps"], []
+        for c in (1, 2, 13, 7, 301):
+            c = min(c, left)
+            cuts.append(c)
+            left -= c
+        cuts.append(left)
+    check(sim, golden, tag, chunks=cuts)
+    sim.close()
+
+
+def test_solo_engine_is_opt_in(golden, monkeypatch):
+    tag = "vogels_1000_s99_t3000_h0_d0"
+    sim = build(golden["meta"]["runs"][tag], {}, monkeypatch)
+    assert sim.engine != "solo"
     check(sim, golden, tag)
     sim.close()

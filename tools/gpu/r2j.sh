@@ -1,1 +1,1 @@
-timeout 300 compute-sanitizer --print-limit 5 python tools/repro_win.py > gpurun_out/r2j.txt 2>&1
+timeout 300 python tools/repro_win.py > gpurun_out/r2j.txt 2>&1
