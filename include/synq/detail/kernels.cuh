@@ -82,6 +82,7 @@ struct engine_state {
     uint32_t* expiring;
     uint32_t* expiring_count;
     uint8_t* caught;              // k_catchup1 (mode 0): ages advance to t + 1 in the next k_update
+    unsigned long long* split_param;  // split catch-up: [0] = t, [1] = expiring count (written by part 1)
     const uint8_t* row_plastic;   // models with plastic(): row holds a plastic synapse (else nullptr)
 
     unsigned long long* counters;
@@ -551,15 +552,26 @@ struct catchup_list {
     const uint32_t* frame = nullptr;
     uint32_t ntr = 0, total = 0;
     int64_t through = 0;
-    SYNQ_DEV void load(const engine_state<M>& st, int mode, int64_t t) {
+    // part 0: the whole list; 1: frame(due) only; 2: the expiring neurons
+    // only, with t and their count from split_param (written by part 1: the
+    // expiring part may run beside the receive, whose epilogue advances t)
+    int part = 0;
+    SYNQ_DEV void load(const engine_state<M>& st, int mode, int64_t t, int part_ = 0) {
+        part = part_;
         through = mode == 0 ? t : t - 1;
+        if (mode == 0 && part == 2) {
+            frame = nullptr;
+            ntr = 0;
+            total = static_cast<uint32_t>(st.split_param[1]);
+            return;
+        }
         if (mode == 0) {
             const int64_t due = t - static_cast<int64_t>(st.delay) + 1;
             if (due >= 0) {
                 frame = st.queue + static_cast<uint64_t>(due % st.Q) * st.n;
                 ntr = st.qcount[due % st.Q];
             }
-            total = ntr + *st.expiring_count;
+            total = part == 1 ? ntr : ntr + *st.expiring_count;
         } else {
             total = st.n;
             ntr = 0;
@@ -567,7 +579,9 @@ struct catchup_list {
         }
     }
     SYNQ_DEV uint32_t at(const engine_state<M>& st, int mode, uint32_t k) const {
-        return mode == 1 ? k : (k < ntr ? frame[k] : st.expiring[k - ntr]);
+        if (mode == 1) return k;
+        if (part == 2) return st.expiring[k];
+        return k < ntr ? frame[k] : st.expiring[k - ntr];
     }
 };
 
@@ -599,14 +613,18 @@ SYNQ_DEV void replay_window(const M& model, SS& sv, uint64_t prew, uint64_t post
 }
 
 template <class M, bool kCompact = false>
-__global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st, int mode) {
+__global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st, int mode, int part) {
     using SF = typename synapse_fields_of<M>::type;
     constexpr int U = 4;  // synapses per thread, loads batched
     grid_launch_dependents();  // k_recv_win may start its prologue on SMs this grid frees
-    const int64_t t = *st.t_dev;
+    const int64_t t = part == 2 ? static_cast<int64_t>(st.split_param[0]) : *st.t_dev;
+    if (part == 1 && blockIdx.x == 0 && threadIdx.x == 0) {  // parameters of the expiring part
+        st.split_param[0] = static_cast<unsigned long long>(t);
+        st.split_param[1] = *st.expiring_count;
+    }
     if constexpr (kCompact) compact_tiles<M, 256>(st, t);
     catchup_list<M> cl;
-    cl.load(st, mode, t);  // (k_update counts the expiring neurons)
+    cl.load(st, mode, t, part);  // (k_update counts the expiring neurons)
     const int64_t through = cl.through;
     // work item = (neuron, chunk of U x 32 synapses), one per warp: many
     // items' load chains in flight per SM; ages advance later

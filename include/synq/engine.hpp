@@ -205,6 +205,12 @@ public:
             if (stream_) cudaStreamSynchronize(stream_);
             detail::nccl_comm_destroy(nccl_);
         }
+        if (side_) {
+            cudaStreamSynchronize(side_);
+            cudaStreamDestroy(side_);
+        }
+        if (fork_ev_) cudaEventDestroy(fork_ev_);
+        if (join_ev_) cudaEventDestroy(join_ev_);
         if (stream_) {
             cudaStreamSynchronize(stream_);
             cudaStreamDestroy(stream_);
@@ -713,6 +719,19 @@ private:
         build_splits(graph_, lo, win_split_, stream_);
         win_ = dev::recv_win{win_lo_dev_.get(), win_split_.get(), C, wmax, static_cast<uint32_t>(ecap)};
         win_on_ = true;
+        if constexpr (has_synapses) {
+            // opt-in: at Brunel+ 1e8 the receive's whole-SM CTAs wait for the
+            // side stream's CTAs (39.4 vs 35.1 us per step); 1e9: 203.6 vs 207
+            bool split = false;
+            if (const char* e = std::getenv("SYNQ_SPLIT_CATCHUP")) split = std::atoi(e) != 0;
+            if (split && hist_words_ == 1) {
+                SYNQ_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+                SYNQ_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+                SYNQ_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
+                split_param_.resize(2);
+                split_catchup_ = true;
+            }
+        }
     }
 
     // ---- partition helpers (setup_persistent; shard construction)
@@ -1096,6 +1115,7 @@ private:
         s.hist_words = hist_words_;
         s.ages = ages_.get();
         s.caught = caught_ ? caught_.get() : nullptr;
+        s.split_param = split_param_ ? split_param_.get() : nullptr;
         s.row_plastic = row_plastic_ ? row_plastic_.get() : nullptr;
         s.expiring = expiring_.get();
         s.expiring_count = expiring_count_.get();
@@ -1351,11 +1371,22 @@ private:
             if (hist_words_ == 1) {
                 // warp items; 4 CTAs of 8 warps per SM (60 registers)
                 uint32_t g = static_cast<uint32_t>(sms_) * 4;
+                // mode 0 with a side stream: frame(due) here (the receive
+                // needs its synapses), the expiring neurons on side_ beside
+                // the receive (disjoint rows: expiring = not transmitting)
+                const int part = (mode == 0 && split_catchup_) ? 1 : 0;
                 if (fuse_compact) {
                     g = std::max(g, ntiles_update_);
-                    dev::k_catchup1<Model, true><<<g, 256, 0, stream_>>>(model_, state(), mode);
+                    dev::k_catchup1<Model, true><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
                 } else {
-                    dev::k_catchup1<Model, false><<<g, 256, 0, stream_>>>(model_, state(), mode);
+                    dev::k_catchup1<Model, false><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
+                }
+                if (part == 1) {
+                    SYNQ_CUDA(cudaEventRecord(fork_ev_, stream_));
+                    SYNQ_CUDA(cudaStreamWaitEvent(side_, fork_ev_, 0));
+                    dev::k_catchup1<Model, false><<<uint32_t(sms_) * 4, 256, 0, side_>>>(model_, state(), mode, 2);
+                    SYNQ_CUDA(cudaEventRecord(join_ev_, side_));
+                    join_pending_ = true;
                 }
                 if (mode == 1)  // (mode 0: the next k_update advances the caught neurons' ages)
                     dev::k_catchup_ages<Model><<<std::max<uint32_t>(1, std::min<uint32_t>((n_ + 255) / 256, sms_)), 256, 0,
@@ -1405,6 +1436,10 @@ private:
             dev::k_det_apply<Model, kReceiveBlock><<<grid_for(n_, kReceiveBlock), kReceiveBlock, 0, stream_>>>(model_, st);
         } else {
             dev::k_receive<Model, kReceiveBlock><<<rgrid, kReceiveBlock, 0, stream_>>>(model_, st);
+        }
+        if (join_pending_) {  // the next step starts after the side stream's expiring catch-up
+            SYNQ_CUDA(cudaStreamWaitEvent(stream_, join_ev_, 0));
+            join_pending_ = false;
         }
     }
 
@@ -1578,7 +1613,8 @@ private:
         const bool win = win_on_ && (exact_ || !atomic_recv_);
         const bool compact = ntiles_update_ <= kCompactTiles;
         const bool fuse = compact && has_synapses && hist_words_ == 1 && delay_ >= 2 && !opt_.debug_checks;
-        return 2 + (compact && !fuse ? 1 : 0) + (has_synapses ? 1 : 0) + (!win && exact_ ? 3 : 0) +
+        return 2 + (compact && !fuse ? 1 : 0) + (has_synapses ? (split_catchup_ ? 2 : 1) : 0) +
+               (!win && exact_ ? 3 : 0) +
                (opt_.debug_checks ? 1 : 0);
     }
 
@@ -1708,6 +1744,11 @@ private:
     dev_array<unsigned long long> counters_dev_, tile_status_, log_cursor_;
     dev_array<uint32_t> tile_bal_;
     dev_array<uint8_t> caught_, row_plastic_;
+    // split catch-up (SYNQ_SPLIT_CATCHUP=1, with the windowed receive)
+    dev_array<unsigned long long> split_param_;
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
+    bool split_catchup_ = false, join_pending_ = false;
     dev_array<uint32_t> tile_ctr_, done_ctr_, flags_;
     uint32_t ntiles_update_ = 1;
     dev_array<int64_t> t_dev_, t0_dev_;
