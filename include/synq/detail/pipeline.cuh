@@ -56,6 +56,7 @@ namespace synq::dev {
 constexpr int kPipeThreads = 512;
 constexpr int kStreamChunks = 64;  // streamed update: up to 64 x UT neurons per CTA
 constexpr int kPipeMaxBatch = 8;  // frames per delivery pass (group ids frame * 4 + class < 32)
+constexpr int kEllSpt = 4;        // ELL delivery: spikes per thread per iteration
 
 SYNQ_DEV uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 SYNQ_DEV void st_release_cta(uint32_t* p, uint32_t v) {
@@ -898,43 +899,67 @@ __global__ void __launch_bounds__(NT, 1)
                     if (profiling) mark(P_DELIVER);
                 }
             } else {
-                for (uint32_t g0 = 0; g0 < S; g0 += DT) {
-                    // one spike per thread: id, this CTA's row window, chunk count
-                    const uint32_t g = g0 + dtid;
-                    uint32_t nchunk = 0, sb = 0, se = 0, base = 0, row4 = 0;
-                    if (g < S) {
-                        uint32_t w = 0, fw = 0;
-    #pragma unroll
-                        for (int q = 1; q < MB; ++q)
-                            if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
-                                w = q;
-                                fw = fpre[q];
-                            }
-                        const uint32_t gl = g - fw;
-                        const uint32_t* seg = s_seg[w];
-                        const uint32_t a = piece_of(seg, P, gl);
-                        const uint32_t src = __ldcg(ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
-                        if (w >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = src;
-                        const uint32_t* sp = ps.split + static_cast<uint64_t>(src) * (C + 1) + c;
-                        sb = __ldg(sp);
-                        se = __ldg(sp + 1);
-                        my_deliv += se - sb;
-                        row4 = src * pitch4;
-                        base = s_cbase[w] + static_cast<uint32_t>(source_class(ps, src)) * ps.win_cap;
-                        nchunk = se > sb ? ((se + 3) >> 2) - (sb >> 2) : 0;
+                for (uint32_t g0 = 0; g0 < S; g0 += DT * kEllSpt) {
+                    // kEllSpt spikes per thread (loads of all of them in
+                    // flight together): id, this CTA's row window, chunks
+                    uint32_t nch[kEllSpt], sbv[kEllSpt], sev[kEllSpt], basev[kEllSpt], srcv[kEllSpt];
+                    uint32_t nchunk = 0;
+#pragma unroll
+                    for (int u = 0; u < kEllSpt; ++u) {
+                        const uint32_t g = g0 + u * DT + dtid;
+                        srcv[u] = 0xffffffffu;
+                        basev[u] = 0;
+                        if (g < S) {
+                            uint32_t w = 0, fw = 0;
+#pragma unroll
+                            for (int q = 1; q < MB; ++q)
+                                if (static_cast<uint32_t>(q) < B && fpre[q] <= g) {
+                                    w = q;
+                                    fw = fpre[q];
+                                }
+                            const uint32_t gl = g - fw;
+                            const uint32_t* seg = s_seg[w];
+                            const uint32_t a = piece_of(seg, P, gl);
+                            srcv[u] = __ldcg(ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
+                            basev[u] = s_cbase[w];
+                            if (w >= wlog && lbase + g < ps.log_cap) ps.log[lbase + g] = srcv[u];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kEllSpt; ++u) {
+                        sbv[u] = sev[u] = 0;
+                        if (srcv[u] != 0xffffffffu) {
+                            const uint32_t* sp = ps.split + static_cast<uint64_t>(srcv[u]) * (C + 1) + c;
+                            sbv[u] = __ldg(sp);
+                            sev[u] = __ldg(sp + 1);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kEllSpt; ++u) {
+                        nch[u] = sev[u] > sbv[u] ? ((sev[u] + 3) >> 2) - (sbv[u] >> 2) : 0;
+                        nchunk += nch[u];
+                        my_deliv += sev[u] - sbv[u];
+                        if (srcv[u] != 0xffffffffu)
+                            basev[u] += static_cast<uint32_t>(source_class(ps, srcv[u])) * ps.win_cap;
                     }
                     uint32_t total;
                     const uint32_t first = group_exclusive_scan<DT, UW, BAR_D>(nchunk, s_dtmp, total);
                     if (profiling) mark(P_GATHER);
                     for (uint32_t i0 = 0; i0 < total; i0 += cap) {
                         // chunk list: {16-byte chunk index, ring base << 5 | hi << 2 | lo}
-                        for (uint32_t q = 0; q < nchunk; ++q) {
-                            const uint32_t it = first + q;
-                            if (it < i0 || it >= i0 + cap) continue;
-                            const uint32_t w0 = ((sb >> 2) + q) << 2;  // first word of the chunk
-                            const uint32_t lo = sb > w0 ? sb - w0 : 0;
-                            const uint32_t hi = min(4u, se - w0);
-                            chunks[it - i0] = make_uint2(row4 + (sb >> 2) + q, (base << 5) | (hi << 2) | lo);
+                        uint32_t off = first;
+#pragma unroll
+                        for (int u = 0; u < kEllSpt; ++u) {
+                            const uint32_t sb = sbv[u], se = sev[u], row4 = srcv[u] * pitch4, base = basev[u];
+                            for (uint32_t q = 0; q < nch[u]; ++q) {
+                                const uint32_t it = off + q;
+                                if (it < i0 || it >= i0 + cap) continue;
+                                const uint32_t w0 = ((sb >> 2) + q) << 2;  // first word of the chunk
+                                const uint32_t lo = sb > w0 ? sb - w0 : 0;
+                                const uint32_t hi = min(4u, se - w0);
+                                chunks[it - i0] = make_uint2(row4 + (sb >> 2) + q, (base << 5) | (hi << 2) | lo);
+                            }
+                            off += nch[u];
                         }
                         named_bar(BAR_D, DT);
                         if (profiling) mark(11);
