@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(NT, 1)
             // ---- poll: warp w takes frame rel r_next + w (warp 0 waits)
             // (frame f is taken once frame f + lag is complete: the
             // publishers streamed the rows of f into L2 meanwhile)
-            if (dwarp < static_cast<uint32_t>(MB)) {
+            if (dwarp < min(static_cast<uint32_t>(MB), ps.max_pass)) {
                 const uint32_t r = r_next + dwarp;
                 bool ok = false;
                 if (dwarp == 0) {
@@ -776,25 +776,21 @@ __global__ void __launch_bounds__(NT, 1)
                 const uint4* bmw = ps.bm + static_cast<uint64_t>(c) * WQ;
                 for (uint32_t g0 = 0; g0 < S; g0 += cap) {
                     const uint32_t n = min(cap, S - g0);
-                    // (1) spike ids: one item per (frame, piece); a piece's ids
-                    // are contiguous in the queue slice and in the pass, so no
-                    // search is needed.  Every thread issues all its 4-byte
-                    // global->shared copies (cp.async), then one wait.
+                    // (1) spike ids: one per thread and pass position (its
+                    // frame by the pass prefix, its piece by binary search
+                    // over the frame's piece prefix); every thread issues
+                    // its 4-byte global->shared copies (cp.async), one wait
+                    for (uint32_t i = dtid; i < n; i += DT) {
+                        const uint32_t g = g0 + i;
+                        uint32_t w = 0;
 #pragma unroll
-                    for (int w = 0; w < MB; ++w) {
-                        if (static_cast<uint32_t>(w) >= B) break;
+                        for (int q = 1; q < MB; ++q)
+                            if (static_cast<uint32_t>(q) < B && fpre[q] <= g) w = q;
+                        const uint32_t gl = g - fpre[w];
                         const uint32_t* seg = s_seg[w];
-                        const uint32_t qb = s_qbase[w], fb0 = fpre[w];
-                        if (fb0 + seg[P] <= g0 || fb0 >= g0 + n) continue;  // frame outside this chunk
-                        for (uint32_t a = dtid; a < P; a += DT) {
-                            const uint32_t o0 = seg[a], o1 = seg[a + 1];
-                            for (uint32_t o = o0; o < o1; ++o) {
-                                const uint32_t gg = fb0 + o;
-                                if (gg < g0 || gg >= g0 + n) continue;
-                                cp_async4(s_src + (gg - g0), ps.queue + qb + s_lo[a] + (o - o0));
-                                s_grp[gg - g0] = static_cast<uint8_t>(w);
-                            }
-                        }
+                        const uint32_t a = piece_of(seg, P, gl);
+                        cp_async4(s_src + i, ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
+                        s_grp[i] = static_cast<uint8_t>(w);
                     }
                     cp_async_wait_all();
                     named_bar(BAR_D, DT);
