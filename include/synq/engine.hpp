@@ -50,6 +50,7 @@
 #include "synq/detail/persistent.cuh"
 #include "synq/detail/pipeline.cuh"
 #include "synq/detail/solo.cuh"
+#include "synq/detail/cluster.cuh"
 #include "synq/detail/exchange.hpp"
 #include "synq/models/benchmarks.hpp"
 #include "synq/network_desc.hpp"
@@ -395,6 +396,7 @@ public:
     bool persistent() const { return persistent_; }
     bool pipelined() const { return persistent_ && pipe_; }
     bool solo() const { return persistent_ && solo_; }
+    bool cluster() const { return persistent_ && cluster_; }
     bool bitmap_delivery() const { return persistent_ && pipe_ && pipe_bm_; }
     bool exact() const { return exact_ || persistent_ || (win_on_ && !atomic_recv_); }
     uint64_t construction_fixups() const { return graph_.tie_fixups; }
@@ -848,10 +850,20 @@ private:
                     (opt_.tiles == 0 || opt_.tiles == 1) && opt_.pipeline < 0 && !std::getenv("SYNQ_PIPELINE");
         const char* solo_env = std::getenv("SYNQ_SOLO");
         solo = solo && solo_env && std::atoi(solo_env) != 0;
-        uint32_t C = solo ? 1u : (opt_.tiles ? opt_.tiles : tiles_for(n_));
+        // SYNQ_CLUSTER=1: one thread-block cluster owns the network
+        // (detail/cluster.cuh), frames through distributed shared memory
+        bool clus = !solo && W == 1 && !opt_.shard_nccl && n_ <= dev::kClusterMaxNeurons &&
+                    delay_ <= dev::kClusterMaxDelay && opt_.tiles == 0 && opt_.pipeline < 0 &&
+                    !std::getenv("SYNQ_PIPELINE");
+        const char* clus_env = std::getenv("SYNQ_CLUSTER");
+        clus = clus && clus_env && std::atoi(clus_env) != 0 && !cluster_failed_;
+        uint32_t CLn = 16;
+        if (const char* e = std::getenv("SYNQ_CLUSTER_SIZE")) CLn = static_cast<uint32_t>(std::atoi(e));
+        if (clus && (CLn < 2 || CLn > 16 || n_ > CLn * 2 * dev::kClusterThreads)) clus = false;
+        uint32_t C = solo ? 1u : (clus ? CLn : (opt_.tiles ? opt_.tiles : tiles_for(n_)));
         C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), n_});
         const uint32_t max_local = 4 * NTH;  // register-resident state: <= 4 neurons per thread
-        if (!solo && uint64_t(C) * max_local < n_)
+        if (!solo && !clus && uint64_t(C) * max_local < n_)
             C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (n_ + max_local - 1) / max_local));
         // shards: contiguous rank ranges of the receiving region (by receive
         // cost) and of the update-only region (by count); then this rank's
@@ -913,7 +925,18 @@ private:
         SYNQ_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         size_t smem = 0;
         solo_ = false;
-        if (solo) {
+        cluster_ = false;
+        if (clus) {
+            smem = dev::cluster_smem_bytes(uint32_t(K), wcap, n_, delay_, C);
+            if (C != CLn || longest > 2 * uint32_t(dev::kClusterThreads) || smem + 16 * 1024 > size_t(max_smem)) {
+                cluster_failed_ = true;  // the multi-CTA engines instead
+                return setup_persistent();
+            }
+            cluster_ = true;
+            pipe_ = false;
+            pipe_bm_ = false;
+            npt_ = longest <= uint32_t(dev::kClusterThreads) ? 1 : 2;
+        } else if (solo) {
             if (C != 1) throw device_error("internal: single-CTA engine with several pieces");
             smem = dev::solo_smem_bytes(uint32_t(K), wcap, n_);
             if (smem + 16 * 1024 > size_t(max_smem) || longest > dev::kSoloMaxNeurons) return;
@@ -944,6 +967,27 @@ private:
         int per_sm = 0;
         SYNQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(kernel_threads()), smem));
         if (per_sm < 1) return;
+        if (cluster_) {  // the whole cluster must be schedulable (16 CTAs: non-portable size)
+            if (C > 8) SYNQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(C);
+            cfg.blockDim = dim3(kernel_threads());
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = C;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclus = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclus, fn, &cfg) != cudaSuccess || nclus < 1) {
+                cudaGetLastError();
+                cluster_ = false;
+                cluster_failed_ = true;
+                return setup_persistent();
+            }
+        }
         if (opt_.profile) {
             prof_.resize(size_t(C) * dev::P_SLOTS);
             prof_.zero(stream_);
@@ -1276,12 +1320,39 @@ private:
         }
     }
 
+    // the persistent step kernel: cooperative launch (all CTAs co-resident),
+    // or one thread-block cluster (the cluster engine)
+    void launch_step_kernel(void** args) requires population_model {
+        if (cluster_) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(tiles_);
+            cfg.blockDim = dim3(kernel_threads());
+            cfg.dynamicSmemBytes = smem_;
+            cfg.stream = stream_;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = tiles_;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            SYNQ_CUDA(cudaLaunchKernelExC(&cfg, kernel_fn(), args));
+        } else {
+            SYNQ_CUDA(cudaLaunchCooperativeKernel(kernel_fn(), dim3(tiles_), dim3(kernel_threads()), args, smem_,
+                                                  stream_));
+        }
+    }
+
     uint32_t kernel_threads() const {
+        if (cluster_) return static_cast<uint32_t>(dev::kClusterThreads);
         if (solo_) return static_cast<uint32_t>(dev::kSoloThreads);
         return pipe_ ? pipe_threads_ : static_cast<uint32_t>(dev::kPersistThreads);
     }
 
     const void* kernel_fn() const requires population_model {
+        if (cluster_)
+            return npt_ == 1 ? reinterpret_cast<const void*>(dev::k_cluster<Model, 1>)
+                             : reinterpret_cast<const void*>(dev::k_cluster<Model, 2>);
         if (solo_)
             return npt_ == 1 ? reinterpret_cast<const void*>(dev::k_solo<Model, 1>)
                              : (npt_ == 2 ? reinterpret_cast<const void*>(dev::k_solo<Model, 2>)
@@ -1471,8 +1542,7 @@ private:
                 int32_t nsteps = static_cast<int32_t>(b);
                 Model m = model_;
                 void* args[] = {&m, &ps, &t0, &nsteps};
-                SYNQ_CUDA(cudaLaunchCooperativeKernel(kernel_fn(), dim3(tiles_),
-                                                      dim3(kernel_threads()), args, smem_, stream_));
+                launch_step_kernel(args);
                 launches_ += 1;
             }
         } else {
@@ -1566,8 +1636,7 @@ private:
             int32_t nsteps = static_cast<int32_t>(b);
             Model m = model_;
             void* args[] = {&m, &ps, &t0, &nsteps};
-            SYNQ_CUDA(cudaLaunchCooperativeKernel(kernel_fn(), dim3(tiles_), dim3(kernel_threads()), args, smem_,
-                                                  stream_));
+            launch_step_kernel(args);
             SYNQ_CUDA(cudaGetLastError());
             launches_ += 1;
             if (opt_.debug_checks) {
@@ -1818,6 +1887,8 @@ private:
     bool pipe_ = false;  // pipelined kernel (detail/pipeline.cuh)
     bool pipe_bm_ = false;  // ... with bitmap delivery
     bool solo_ = false;     // single-CTA engine (detail/solo.cuh)
+    bool cluster_ = false;  // one-cluster engine (detail/cluster.cuh)
+    bool cluster_failed_ = false;
     dev_array<uint4> bm_;
     uint32_t bm_wq_ = 0, bm_row4_ = 0;
     uint32_t pipe_uw_ = 4, pipe_npt_ = 1, ring_R_ = 0, lead_ = 0, lag_ = 0, pf_cap_ = 0;

@@ -292,7 +292,7 @@ class Sim:
 
     @property
     def engine(self) -> str:
-        return {0: "graph", 1: "persistent", 2: "pipelined", 3: "pipelined-bitmap", 4: "solo"}[
+        return {0: "graph", 1: "persistent", 2: "pipelined", 3: "pipelined-bitmap", 4: "solo", 5: "cluster"}[
             lib().synq_sim_engine(self.h)]
 
     @property

@@ -63,6 +63,7 @@ public:
     virtual bool persistent() const = 0;
     virtual bool pipelined() const = 0;
     virtual bool solo() const = 0;
+    virtual bool cluster() const = 0;
     virtual bool bitmap_delivery() const = 0;
     virtual bool exact() const = 0;
     virtual const std::vector<uint32_t>& step_spikes() const = 0;
@@ -202,6 +203,7 @@ public:
     bool persistent() const override { return net_->persistent(); }
     bool pipelined() const override { return net_->pipelined(); }
     bool solo() const override { return net_->solo(); }
+    bool cluster() const override { return net_->cluster(); }
     bool bitmap_delivery() const override { return net_->bitmap_delivery(); }
     bool exact() const override { return net_->exact(); }
     const std::vector<uint32_t>& step_spikes() const override { return net_->step_spike_counts(); }
@@ -781,6 +783,7 @@ synq_status synq_sim_phase_cycles(const synq_sim* s, double out[15], uint32_t* t
 int synq_sim_engine(const synq_sim* s) {
     if (!s || !s->impl->persistent()) return 0;
     if (s->impl->solo()) return 4;
+    if (s->impl->cluster()) return 5;
     return s->impl->bitmap_delivery() ? 3 : (s->impl->pipelined() ? 2 : 1);
 }
 int synq_sim_exact(const synq_sim* s) { return s && s->impl->exact() ? 1 : 0; }

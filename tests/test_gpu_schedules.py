@@ -25,7 +25,7 @@ pytestmark = pytest.mark.gpu
 
 
 def build(m, env, monkeypatch, **kw):
-    for k in ("SYNQ_BITMAP", "SYNQ_UW", "SYNQ_LAG", "SYNQ_LEAD", "SYNQ_PREFETCH", "SYNQ_STREAM", "SYNQ_WORKQ", "SYNQ_SOLO"):
+    for k in ("SYNQ_BITMAP", "SYNQ_UW", "SYNQ_LAG", "SYNQ_LEAD", "SYNQ_PREFETCH", "SYNQ_STREAM", "SYNQ_WORKQ", "SYNQ_SOLO", "SYNQ_CLUSTER", "SYNQ_CLUSTER_SIZE"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, str(v))
@@ -172,4 +172,27 @@ def test_solo_engine_is_opt_in(golden, monkeypatch):
     sim = build(golden["meta"]["runs"][tag], {}, monkeypatch)
     assert sim.engine != "solo"
     check(sim, golden, tag)
+    sim.close()
+
+
+@pytest.mark.parametrize("tag", ["brunel_2000_s99_t3000_h0_d0", "vogels_1000_s99_t3000_h0_d0",
+                                 "vogels_500_s3_t500_h0_d3", "vogels_4000_s1_t10000_h0_d0"])
+@pytest.mark.parametrize("size", [8, 16])
+@pytest.mark.parametrize("chunks", [None, "uneven"])
+def test_cluster_engine_bit_exact(golden, monkeypatch, tag, size, chunks):
+    """One thread-block cluster (detail/cluster.cuh, SYNQ_CLUSTER=1): frames
+    through distributed shared memory, bit-exact; uneven run() chunks make
+    launches start from frames of an earlier launch."""
+    m = golden["meta"]["runs"][tag]
+    sim = build(m, {"SYNQ_CLUSTER": 1, "SYNQ_CLUSTER_SIZE": size}, monkeypatch)
+    assert sim.engine == "cluster", sim.engine
+    cuts = None
+    if chunks:
+        left, cuts = m["steps"], []
+        for c in (1, 2, 13, 7, 301):
+            c = min(c, left)
+            cuts.append(c)
+            left -= c
+        cuts.append(left)
+    check(sim, golden, tag, chunks=cuts)
     sim.close()
