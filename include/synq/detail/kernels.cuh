@@ -270,6 +270,8 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
     const uint32_t i = tile * BLOCK + threadIdx.x;
 
     bool spk = false;
+    unsigned long long n_exp = 0, n_upd = 0;  // expiring neurons, retired non-plastic synapse updates
+    bool listed = false;                      // expiring with a plastic row: catch-up list
     if (i < st.n) {
         values_t<NF> v;
         load_all(st.nf, i, v);
@@ -295,23 +297,36 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
             const bool transmits = (st.delay == 1) ? spk : hist_bit(st, i, t - st.delay + 1);
             const int64_t a = st.ages[i];
             if (!transmits && a + st.history <= t + st.delay + 1) {
-                atomicAdd(&st.counters[C_EXPIRY], 1ull);  // expiry_batches (engine.hpp:349)
+                n_exp = 1;  // expiry_batches (engine.hpp:349), summed per warp below
                 if (st.row_plastic && !st.row_plastic[i]) {
                     // no plastic synapse in the row: the catch-up through t is
                     // only its counter and age (no replay, not listed)
                     if (a <= t) {
-                        atomicAdd(&st.counters[C_SYN_UPDATES],
-                                  static_cast<unsigned long long>(st.degree[i]) * static_cast<unsigned long long>(t - a + 1));
+                        n_upd = static_cast<unsigned long long>(st.degree[i]) * static_cast<unsigned long long>(t - a + 1);
                         st.ages[i] = static_cast<uint32_t>(t + 1);
                     }
                 } else {
-                    const uint32_t slot = atomicAdd(st.expiring_count, 1u);
-                    st.expiring[slot] = i;
+                    listed = true;
                 }
             }
         }
     }
 
+    if constexpr (kSyn) {  // one atomic per warp, not per neuron (one counter word for the whole grid)
+        const unsigned lm = __ballot_sync(0xffffffffu, listed);
+        if (lm) {  // the expiring list, appended per warp (its order does not matter)
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(st.expiring_count, static_cast<uint32_t>(__popc(lm)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (listed) st.expiring[base + __popc(lm & ((1u << lane) - 1u))] = i;
+        }
+        for (int o = 16; o; o >>= 1) {
+            n_exp += __shfl_xor_sync(0xffffffffu, n_exp, o);
+            n_upd += __shfl_xor_sync(0xffffffffu, n_upd, o);
+        }
+        if (lane == 0 && n_exp) atomicAdd(&st.counters[C_EXPIRY], n_exp);
+        if (lane == 0 && n_upd) atomicAdd(&st.counters[C_SYN_UPDATES], n_upd);
+    }
     // ordered compaction: warp ballots -> block scan -> look-back across tiles
     const unsigned ball = __ballot_sync(0xffffffffu, spk);
     if (lane == 0) s_warp[warp] = __popc(ball);
