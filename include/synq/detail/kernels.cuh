@@ -627,10 +627,10 @@ SYNQ_DEV void replay_window(const M& model, SS& sv, uint64_t prew, uint64_t post
     }
 }
 
-template <class M, bool kCompact = false>
-__global__ void __launch_bounds__(256, 4) k_catchup1(M model, engine_state<M> st, int mode, int part) {
+// U: synapses per lane (loads batched); MINB: CTAs per SM the registers allow
+template <class M, bool kCompact = false, int U = 4, int MINB = 4>
+__global__ void __launch_bounds__(256, MINB) k_catchup1(M model, engine_state<M> st, int mode, int part) {
     using SF = typename synapse_fields_of<M>::type;
-    constexpr int U = 4;  // synapses per thread, loads batched
     grid_launch_dependents();  // k_recv_win may start its prologue on SMs this grid frees
     const int64_t t = part == 2 ? static_cast<int64_t>(st.split_param[0]) : *st.t_dev;
     if (part == 1 && blockIdx.x == 0 && threadIdx.x == 0) {  // parameters of the expiring part

@@ -685,6 +685,7 @@ private:
         if (const char* e = std::getenv("SYNQ_WINRECV"); e && std::atoi(e) == 0) return;
         if (const char* e = std::getenv("SYNQ_ATOMIC_RECV")) atomic_recv_ = std::atoi(e) != 0;
         if (const char* e = std::getenv("SYNQ_PDL")) pdl_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SYNQ_CATCHUP_U")) catchup_u_ = std::atoi(e);
         if (n_ == 0 || graph_.edges == 0 || graph_.deg_max >= (1u << 24) || !graph_.cells) return;
         const uint32_t cap_t = uint32_t(dev::kWinTPT) * kWinBlock;
         const std::vector<uint32_t> indeg = in_degrees(graph_, stream_);
@@ -1446,11 +1447,20 @@ private:
                 // needs its synapses), the expiring neurons on side_ beside
                 // the receive (disjoint rows: expiring = not transmitting)
                 const int part = (mode == 0 && split_catchup_) ? 1 : 0;
+                // SYNQ_CATCHUP_U=2: 2 synapses per lane, 6 CTAs per SM (A/B)
+                const bool u2 = catchup_u_ == 2;
+                if (u2) g = static_cast<uint32_t>(sms_) * 6;
                 if (fuse_compact) {
                     g = std::max(g, ntiles_update_);
-                    dev::k_catchup1<Model, true><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
+                    if (u2)
+                        dev::k_catchup1<Model, true, 2, 6><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
+                    else
+                        dev::k_catchup1<Model, true><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
                 } else {
-                    dev::k_catchup1<Model, false><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
+                    if (u2)
+                        dev::k_catchup1<Model, false, 2, 6><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
+                    else
+                        dev::k_catchup1<Model, false><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
                 }
                 if (part == 1) {
                     SYNQ_CUDA(cudaEventRecord(fork_ev_, stream_));
@@ -1866,6 +1876,7 @@ private:
     dev_array<uint32_t> win_lo_dev_, win_split_;
     size_t win_smem_ = 0;
     bool win_on_ = false, atomic_recv_ = false, pdl_ = true;
+    int catchup_u_ = 4;
     uint32_t fold_t0_ = 0, fold_t1_ = 0;
     uint32_t win_cap_ = 0, pieces_ = 0, publishers_ = 0, stage_items_ = 0;
     dev_array<uint32_t> piece_src_;

@@ -1,7 +1,7 @@
 # round-2 measurement pass (1 GPU): tests, bench, launch lists, ncu captures, secondary configs
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/f_gpu.txt
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -15 > gpurun_out/f_gputest.txt
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -15 > gpurun_out/f_gputest.txt
 timeout 600 python bench.py > gpurun_out/f_bench.json 2> gpurun_out/f_bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/f_launches.csv python bench.py --steps 1 --warmup 1 --e2e-steps 1 --no-cpu-baseline > gpurun_out/f_bench_ncu.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_pipeline -s 3 -c 1 -o gpurun_out/f_pipe python tools/profile_run.py brunel 1e9 1200 200 > gpurun_out/f_ncu.log 2>&1
