@@ -29,6 +29,7 @@
 #include <cstdint>
 
 #include "synq/detail/device_refs.cuh"
+#include "synq/models/benchmarks.hpp"
 #include "synq/soa.hpp"
 
 namespace synq::dev {
@@ -55,6 +56,16 @@ template <class M>
 constexpr bool model_has_plastic() {
     return requires(const M& m, uint32_t a, uint32_t b) { { m.plastic(a, b) } -> std::convertible_to<bool>; };
 }
+constexpr uint32_t kTraceRing = 128;  // steps of per-neuron trace history (trace-STDP models)
+
+template <class M>
+constexpr bool model_trace_stdp() {
+    if constexpr (requires { trace_stdp<M>::available; })
+        return trace_stdp<M>::available;
+    else
+        return false;
+}
+
 // a model exposing plastic(src, dst) declares update_synapse a no-op for the
 // other synapses (benchmarks.hpp brunel_plus_model): catch-up skips them
 
@@ -83,6 +94,8 @@ struct engine_state {
     uint32_t* expiring_count;
     uint8_t* caught;              // k_catchup1 (mode 0): ages advance to t + 1 in the next k_update
     unsigned long long* split_param;  // split catch-up: [0] = t, [1] = expiring count (written by part 1)
+    float* tr_p;                  // trace-STDP models: P_i(u) at [i * kTraceRing + (u & (kTraceRing - 1))]
+    float* tr_q;                  // ... Q_i(u)
     const uint8_t* row_plastic;   // models with plastic(): row holds a plastic synapse (else nullptr)
 
     unsigned long long* counters;
@@ -288,6 +301,20 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
                                                      : static_cast<uint32_t>(t % (64u * st.hist_words));
             uint64_t* w = st.hist + static_cast<uint64_t>(i) * st.hist_words + (slot >> 6);
             *w = (*w & ~(1ull << (slot & 63))) | (static_cast<uint64_t>(spk) << (slot & 63));
+        }
+        if constexpr (model_trace_stdp<M>()) {
+            if (st.tr_p) {  // the per-neuron traces of step t (the stdp_step float sequence)
+                const stdp_params& sp = trace_stdp<M>::params(model);
+                const uint64_t r0 = static_cast<uint64_t>(i) * kTraceRing;
+                const uint32_t u = static_cast<uint32_t>(t) & (kTraceRing - 1), um = (u - 1) & (kTraceRing - 1);
+                float pt = st.tr_p[r0 + um], qt = st.tr_q[r0 + um];
+                pt *= sp.decay_plus;
+                qt *= sp.decay_minus;
+                if (hist_bit(st, i, t - static_cast<int64_t>(st.delay))) pt += 1.0f;  // pre of this source at t
+                if (spk) qt += 1.0f;                                                 // post of this target at t
+                st.tr_p[r0 + u] = pt;
+                st.tr_q[r0 + u] = qt;
+            }
         }
         if constexpr (kSyn) {  // engine.hpp:318-330
             if (st.caught && st.caught[i]) {  // caught up through t - 1 by the last step's k_catchup1
@@ -713,6 +740,33 @@ __global__ void __launch_bounds__(256, MINB) k_catchup1(M model, engine_state<M>
                 for (int64_t x = a0; x <= through; ++x)
                     model.update_synapse(sv[u], hist_bit(st, nid, x - static_cast<int64_t>(st.delay)),
                                          hist_bit(st, dst[u], x), st.dt);
+            } else if (model_trace_stdp<M>() && st.tr_p) {
+                if constexpr (model_trace_stdp<M>()) {
+                    // the traces are the neurons' P_src / Q_dst (trace_stdp):
+                    // only the weight moves, at the window's events, with the
+                    // decayed traces stdp_step sees there (lif.hpp:78-89)
+                    using T = trace_stdp<M>;
+                    const stdp_params& sp = T::params(model);
+                    const uint64_t rs = static_cast<uint64_t>(nid) * kTraceRing, rd = static_cast<uint64_t>(dst[u]) * kTraceRing;
+                    const uint64_t postu = rotr64(postw[u], r0) & lastn;
+                    float w = sv[u].template get<T::W>();
+                    for (uint64_t ev = prew | postu; ev; ev &= ev - 1) {
+                        const uint32_t e = static_cast<uint32_t>(__ffsll(static_cast<long long>(ev))) - 1;
+                        const uint32_t um = static_cast<uint32_t>(a0 + e - 1) & (kTraceRing - 1);
+                        if ((prew >> e) & 1ull) {
+                            const float qt = st.tr_q[rd + um] * sp.decay_minus;
+                            w = clamp_weight(w - sp.a_minus * qt, sp.w_min, sp.w_max);
+                        }
+                        if ((postu >> e) & 1ull) {
+                            const float pt = st.tr_p[rs + um] * sp.decay_plus;
+                            w = clamp_weight(w + sp.a_plus * pt, sp.w_min, sp.w_max);
+                        }
+                    }
+                    const uint32_t ut = static_cast<uint32_t>(through) & (kTraceRing - 1);
+                    sv[u].template get<T::W>() = w;
+                    sv[u].template get<T::PT>() = st.tr_p[rs + ut];
+                    sv[u].template get<T::QT>() = st.tr_q[rd + ut];
+                }
             } else {
                 replay_window(model, sv[u], prew, rotr64(postw[u], r0) & lastn, n, st.dt);
             }

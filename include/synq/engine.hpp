@@ -261,6 +261,10 @@ public:
             t0 = clock::now();
             ages_.zero(stream_);
             caught_.zero(stream_);
+            if (tr_p_) {
+                tr_p_.zero(stream_);
+                tr_q_.zero(stream_);
+            }
             for (auto& col : syn_cols_) col.zero(stream_);
             if (graph_.edges)
                 dev::k_init_synapses<Model><<<grid_for(uint64_t(n_) * 32, 256), 256, 0, stream_>>>(model_, state());
@@ -625,6 +629,15 @@ private:
             hist_words_ = (history_ + 63) / 64;
             if (hist_words_ > 4) throw std::invalid_argument("history_frames above 256 are not supported");
             hist_.resize(std::max<size_t>(1, size_t(n_) * hist_words_));
+            // trace-STDP models on the one-word-history catch-up: per-neuron
+            // trace rings (SYNQ_TRACE_RINGS=0: replay every synapse step)
+            if constexpr (dev::model_trace_stdp<Model>()) {
+                const char* e = std::getenv("SYNQ_TRACE_RINGS");
+                if (hist_words_ == 1 && (!e || std::atoi(e) != 0)) {
+                    tr_p_.resize(size_t(std::max<uint32_t>(1, n_)) * dev::kTraceRing);
+                    tr_q_.resize(size_t(std::max<uint32_t>(1, n_)) * dev::kTraceRing);
+                }
+            }
         }
         if (!has_synapses && opt_.debug_checks) {  // debug_checks tracks spike bits for every model
             history_ = delay_ + 1;
@@ -1161,6 +1174,8 @@ private:
         s.ages = ages_.get();
         s.caught = caught_ ? caught_.get() : nullptr;
         s.split_param = split_param_ ? split_param_.get() : nullptr;
+        s.tr_p = tr_p_ ? tr_p_.get() : nullptr;
+        s.tr_q = tr_q_ ? tr_q_.get() : nullptr;
         s.row_plastic = row_plastic_ ? row_plastic_.get() : nullptr;
         s.expiring = expiring_.get();
         s.expiring_count = expiring_count_.get();
@@ -1823,6 +1838,7 @@ private:
     dev_array<unsigned long long> counters_dev_, tile_status_, log_cursor_;
     dev_array<uint32_t> tile_bal_;
     dev_array<uint8_t> caught_, row_plastic_;
+    dev_array<float> tr_p_, tr_q_;  // trace-STDP per-neuron trace rings
     // split catch-up (SYNQ_SPLIT_CATCHUP=1, with the windowed receive)
     dev_array<unsigned long long> split_param_;
     cudaStream_t side_ = nullptr;
