@@ -94,7 +94,7 @@ struct engine_state {
     uint32_t* expiring_count;
     uint8_t* caught;              // k_catchup1 (mode 0): ages advance to t + 1 in the next k_update
     unsigned long long* split_param;  // split catch-up: [0] = t, [1] = expiring count (written by part 1)
-    float* tr_p;                  // trace-STDP models: P_i(u) at [i * kTraceRing + (u & (kTraceRing - 1))]
+    float* tr_p;                  // trace-STDP models: P_i(u) at [(u & (kTraceRing - 1)) * n + i]
     float* tr_q;                  // ... Q_i(u)
     const uint8_t* row_plastic;   // models with plastic(): row holds a plastic synapse (else nullptr)
 
@@ -305,15 +305,14 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
         if constexpr (model_trace_stdp<M>()) {
             if (st.tr_p) {  // the per-neuron traces of step t (the stdp_step float sequence)
                 const stdp_params& sp = trace_stdp<M>::params(model);
-                const uint64_t r0 = static_cast<uint64_t>(i) * kTraceRing;
                 const uint32_t u = static_cast<uint32_t>(t) & (kTraceRing - 1), um = (u - 1) & (kTraceRing - 1);
-                float pt = st.tr_p[r0 + um], qt = st.tr_q[r0 + um];
+                float pt = st.tr_p[static_cast<uint64_t>(um) * st.n + i], qt = st.tr_q[static_cast<uint64_t>(um) * st.n + i];
                 pt *= sp.decay_plus;
                 qt *= sp.decay_minus;
                 if (hist_bit(st, i, t - static_cast<int64_t>(st.delay))) pt += 1.0f;  // pre of this source at t
                 if (spk) qt += 1.0f;                                                 // post of this target at t
-                st.tr_p[r0 + u] = pt;
-                st.tr_q[r0 + u] = qt;
+                st.tr_p[static_cast<uint64_t>(u) * st.n + i] = pt;
+                st.tr_q[static_cast<uint64_t>(u) * st.n + i] = qt;
             }
         }
         if constexpr (kSyn) {  // engine.hpp:318-330
@@ -696,7 +695,17 @@ __global__ void __launch_bounds__(256, MINB) k_catchup1(M model, engine_state<M>
         for (int u = 0; u < U; ++u) {
             const uint32_t kk = k0 + u * 32;
             dst[u] = kk < st.pitch ? row[kk] : 0xffffffffu;
-            if (kk < st.deg_max) load_syn(st.sf, static_cast<uint64_t>(nid) * st.deg_max + kk, sv[u]);
+            if (kk < st.deg_max) {
+                const uint64_t si = static_cast<uint64_t>(nid) * st.deg_max + kk;
+                if constexpr (model_trace_stdp<M>()) {
+                    if (st.tr_p)  // the traces come from the rings: only the weight is read
+                        sv[u].template get<trace_stdp<M>::W>() = st.sf.template get<trace_stdp<M>::W>()[si];
+                    else
+                        load_syn(st.sf, si, sv[u]);
+                } else {
+                    load_syn(st.sf, si, sv[u]);
+                }
+            }
         }
         if (!plastic_row && (ch != 0 || lane != 0)) continue;
         if (a0 > through) continue;
@@ -747,30 +756,33 @@ __global__ void __launch_bounds__(256, MINB) k_catchup1(M model, engine_state<M>
                     // decayed traces stdp_step sees there (lif.hpp:78-89)
                     using T = trace_stdp<M>;
                     const stdp_params& sp = T::params(model);
-                    const uint64_t rs = static_cast<uint64_t>(nid) * kTraceRing, rd = static_cast<uint64_t>(dst[u]) * kTraceRing;
+                    const uint64_t rs = nid, rd = dst[u], rn = st.n;  // step-major rings: [slot * n + neuron]
                     const uint64_t postu = rotr64(postw[u], r0) & lastn;
                     float w = sv[u].template get<T::W>();
                     for (uint64_t ev = prew | postu; ev; ev &= ev - 1) {
                         const uint32_t e = static_cast<uint32_t>(__ffsll(static_cast<long long>(ev))) - 1;
                         const uint32_t um = static_cast<uint32_t>(a0 + e - 1) & (kTraceRing - 1);
                         if ((prew >> e) & 1ull) {
-                            const float qt = st.tr_q[rd + um] * sp.decay_minus;
+                            const float qt = st.tr_q[um * rn + rd] * sp.decay_minus;
                             w = clamp_weight(w - sp.a_minus * qt, sp.w_min, sp.w_max);
                         }
                         if ((postu >> e) & 1ull) {
-                            const float pt = st.tr_p[rs + um] * sp.decay_plus;
+                            const float pt = st.tr_p[um * rn + rs] * sp.decay_plus;
                             w = clamp_weight(w + sp.a_plus * pt, sp.w_min, sp.w_max);
                         }
                     }
                     const uint32_t ut = static_cast<uint32_t>(through) & (kTraceRing - 1);
                     sv[u].template get<T::W>() = w;
-                    sv[u].template get<T::PT>() = st.tr_p[rs + ut];
-                    sv[u].template get<T::QT>() = st.tr_q[rd + ut];
+                    sv[u].template get<T::PT>() = st.tr_p[ut * rn + rs];
+                    sv[u].template get<T::QT>() = st.tr_q[ut * rn + rd];
                 }
             } else {
                 replay_window(model, sv[u], prew, rotr64(postw[u], r0) & lastn, n, st.dt);
             }
-            store_syn_changed(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 32, sv[u], s0);
+            if (model_trace_stdp<M>() && st.tr_p)
+                store_syn(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 32, sv[u]);
+            else
+                store_syn_changed(st.sf, static_cast<uint64_t>(nid) * st.deg_max + k0 + u * 32, sv[u], s0);
         }
     }
 }
