@@ -131,6 +131,12 @@ struct engine_state {
 // ------------------------------------------------------------- helpers
 SYNQ_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 
+// programmatic dependent launch (PDL): the primary lets its dependent grid
+// be scheduled early; the dependent waits for the primary's memory before
+// touching its outputs (both are no-ops without the launch attribute)
+SYNQ_DEV void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+SYNQ_DEV void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <class M>
 SYNQ_DEV bool hist_bit(const engine_state<M>& st, uint32_t id, int64_t u) {
     if (u < 0) return false;
@@ -272,6 +278,8 @@ __global__ void __launch_bounds__(BLOCK) k_update(M model, engine_state<M> st) {
     __shared__ uint32_t s_warp[NW];
     __shared__ uint32_t s_meas;
 
+    grid_dependency_wait();    // PDL: the previous step's kernels are complete
+    grid_launch_dependents();  // the catch-up may be scheduled on the SMs this grid frees
     const int64_t t = *st.t_dev;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -580,11 +588,7 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
 // k_catchup, bit for bit.
 SYNQ_DEV uint64_t rotr64(uint64_t x, uint32_t r) { return r ? (x >> r) | (x << (64 - r)) : x; }
 
-// programmatic dependent launch (PDL): the primary lets its dependent grid
-// be scheduled early; the dependent waits for the primary's memory before
-// touching its outputs (both are no-ops without the launch attribute)
-SYNQ_DEV void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-SYNQ_DEV void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 
 // the catch-up list of step t: frame(due) U expiring (mode 0), or every
 // neuron (mode 1, flush through t - 1)
@@ -658,6 +662,7 @@ template <class M, bool kCompact = false, int U = 4, int MINB = 4>
 __global__ void __launch_bounds__(256, MINB) k_catchup1(M model, engine_state<M> st, int mode, int part) {
     using SF = typename synapse_fields_of<M>::type;
     grid_launch_dependents();  // k_recv_win may start its prologue on SMs this grid frees
+    grid_dependency_wait();    // PDL: k_update (and its ballots) are complete
     const int64_t t = part == 2 ? static_cast<int64_t>(st.split_param[0]) : *st.t_dev;
     if (part == 1 && blockIdx.x == 0 && threadIdx.x == 0) {  // parameters of the expiring part
         st.split_param[0] = static_cast<unsigned long long>(t);
@@ -942,6 +947,7 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
     uint32_t* s_ord = s_et + ecap;                         // ecap: events by (target, spike)
     unsigned char* s_syn = reinterpret_cast<unsigned char*>(s_ord + ecap);
 
+    grid_launch_dependents();  // the next step's k_update may be scheduled early (it waits first)
     const int64_t t = *st.t_dev;
     const int64_t due = t - static_cast<int64_t>(st.delay) + 1;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -697,7 +697,10 @@ private:
     void setup_recv_win() {
         if (const char* e = std::getenv("SYNQ_WINRECV"); e && std::atoi(e) == 0) return;
         if (const char* e = std::getenv("SYNQ_ATOMIC_RECV")) atomic_recv_ = std::atoi(e) != 0;
-        if (const char* e = std::getenv("SYNQ_PDL")) pdl_ = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SYNQ_PDL")) {
+            pdl_ = std::atoi(e) != 0;
+            pdl_all_ = std::atoi(e) == 2;
+        }
         if (const char* e = std::getenv("SYNQ_CATCHUP_U")) catchup_u_ = std::atoi(e);
         if (n_ == 0 || graph_.edges == 0 || graph_.deg_max >= (1u << 24) || !graph_.cells) return;
         const uint32_t cap_t = uint32_t(dev::kWinTPT) * kWinBlock;
@@ -1453,6 +1456,21 @@ private:
     // compaction (k_compact) is fused into the catch-up launch when the
     // frame it writes is not the one the catch-up reads (delay >= 2), and the
     // catch-up's ages advance at the start of the windowed receive
+    template <class... KArgs, class... Args>
+    void launch_pdl(void (*kernel)(KArgs...), uint32_t grid, uint32_t block, size_t smem, Args... args) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(block);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream_;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SYNQ_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+    }
+
     void enqueue_catchup(int mode, bool fuse_compact = false) {
         if constexpr (has_synapses) {
             if (hist_words_ == 1) {
@@ -1469,6 +1487,8 @@ private:
                     g = std::max(g, ntiles_update_);
                     if (u2)
                         dev::k_catchup1<Model, true, 2, 6><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
+                    else if (catchup_pdl_ && mode == 0)
+                        launch_pdl(dev::k_catchup1<Model, true>, g, 256, 0, Model(model_), state(), mode, part);
                     else
                         dev::k_catchup1<Model, true><<<g, 256, 0, stream_>>>(model_, state(), mode, part);
                 } else {
@@ -1499,12 +1519,21 @@ private:
         const bool compact = ntiles_update_ <= kCompactTiles;
         const bool win = win_on_ && (exact_ || !atomic_recv_);
         const bool fuse = compact && has_synapses && hist_words_ == 1 && delay_ >= 2 && !opt_.debug_checks;
+        // SYNQ_PDL=2: programmatic dependent launches on every edge of the
+        // step (update, catch-up, receive); measured slower than the receive
+        // edge alone (Brunel+ 1e8: 32.1 vs 31.1 us per step): the early
+        // update / catch-up CTAs wait on SMs the predecessor's tail needs
+        const bool pdl = win && pdl_all_ && has_synapses && hist_words_ == 1 && delay_ >= 2;
         if (compact) {
-            dev::k_update<Model, kUpdateBlock, false><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
+            if (pdl)
+                launch_pdl(dev::k_update<Model, kUpdateBlock, false>, ntiles_update_, kUpdateBlock, 0, Model(model_), st);
+            else
+                dev::k_update<Model, kUpdateBlock, false><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
             if (!fuse) dev::k_compact<Model, kUpdateBlock><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(st);
         } else {
             dev::k_update<Model, kUpdateBlock, true><<<ntiles_update_, kUpdateBlock, 0, stream_>>>(model_, st);
         }
+        catchup_pdl_ = pdl && fuse;
         if (opt_.debug_checks) dev::k_check_frame<Model><<<1, 1024, 0, stream_>>>(st);
         enqueue_catchup(0, fuse);
         const int rgrid = 8 * sms_;
@@ -1893,6 +1922,7 @@ private:
     size_t win_smem_ = 0;
     bool win_on_ = false, atomic_recv_ = false, pdl_ = true;
     int catchup_u_ = 4;
+    bool catchup_pdl_ = false, pdl_all_ = false;
     uint32_t fold_t0_ = 0, fold_t1_ = 0;
     uint32_t win_cap_ = 0, pieces_ = 0, publishers_ = 0, stage_items_ = 0;
     dev_array<uint32_t> piece_src_;
