@@ -102,6 +102,7 @@ struct persist_state {
     uint32_t bm_prefetch;  // stream the bitmap rows of published spikes into L2
     uint32_t stream_mode;  // bitmap delivery: barrier-free work items instead of passes
     uint32_t max_pass;     // frames per delivery pass (<= the polling warps)
+    uint32_t dbg;          // timing experiments only (SYNQ_DBG): bit 1 = bitmap passes skip staging + counting
     // fold table (k_fold_table): tab[n0 * (T1 + 1) + n1] = fl-sum from +0 of
     // n0 copies of delta[0] then n1 copies of delta[1]; nullptr: no table
     const float* fold_tab;

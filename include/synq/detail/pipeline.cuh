@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(NT, 1)
                     if (profiling) mark(P_GATHER);
                     // (2) windows -> shared memory: 16-byte cp.async.cg copies,
                     // all issued back to back, one wait
-                    const uint32_t items = n * WQ;
+                    const uint32_t items = (ps.dbg & 2) ? 0u : n * WQ;
                     for (uint32_t it = dtid; it < items; it += DT) {
                         const uint32_t g = it >> wq_sh, q = it & (WQ - 1);
                         cp_async16_cg(sw + g * WQ + (q ^ ((g >> swz_sh) & swz_m)),
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(NT, 1)
                         if (lane == 31) s_gcp[32] = inc;
                     }
                     named_bar(BAR_D, DT);
-                    const uint32_t nwork = s_gcp[32] << wq_sh;
+                    const uint32_t nwork = (ps.dbg & 2) ? 0u : s_gcp[32] << wq_sh;
                     for (uint32_t it = dwarp; it < nwork; it += DW) {
                         const uint32_t q = it & (WQ - 1), ci = it >> wq_sh;
                         uint32_t G = 0;  // last group with s_gcp[G] <= ci

@@ -1442,6 +1442,8 @@ private:
         if (const char* e = std::getenv("SYNQ_MAXPASS")) p.max_pass = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         p.stream_mode = 0;
         if (const char* e = std::getenv("SYNQ_WORKQ")) p.stream_mode = std::atoi(e) != 0 ? 1u : 0u;
+        p.dbg = 0;
+        if (const char* e = std::getenv("SYNQ_DBG")) p.dbg = static_cast<uint32_t>(std::atoi(e));
         return p;
     }
 
