@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-steps", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the secondary BASELINE configs (Vogels 4000, Brunel+ 1e8) reported beside the headline")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent 1e9-synapse replicas instead of one sharded network")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -293,6 +295,44 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------ B200 arm
+def secondary_configs(synq):
+    """BASELINE configs 1 and 3 measured in the same run (device-timed, after
+    warm-up; not the headline): Vogels-Abbott 4000 over one biological second
+    and Brunel+ 1e8 (STDP) over 0.2 s.  Parity of both: tests/test_gpu_parity*.py."""
+    out = {}
+    try:
+        sim = synq.Sim("vogels", 4000, synq.Opts(seed=1, deterministic=True))
+        sim.run(2000)
+        d0, _ = sim.device_time()
+        c0 = sim.counters()["deliveries"]
+        sim.run(BIO_STEPS)
+        d1, _ = sim.device_time()
+        ev = sim.counters()["deliveries"] - c0
+        out["vogels_4000"] = {"ms_per_bio_s": (d1 - d0) * 1e3, "events_per_s": ev / (d1 - d0),
+                              "engine": sim.engine, "exact": sim.exact}
+        sim.close()
+    except Exception as e:  # reported, never fatal
+        out["vogels_4000"] = {"error": str(e)}
+    try:
+        sim = synq.Sim("brunel+", opts=synq.Opts(seed=1, deterministic=True), synapses=int(1e8))
+        sim.run(500)
+        d0, _ = sim.device_time()
+        c0 = sim.counters()
+        steps = 2000
+        sim.run(steps)
+        d1, _ = sim.device_time()
+        c1 = sim.counters()
+        out["brunel_plus_1e8"] = {"ms_per_bio_s": (d1 - d0) / steps * BIO_STEPS * 1e3,
+                                  "events_per_s": (c1["deliveries"] - c0["deliveries"]) / (d1 - d0),
+                                  "synapse_updates_per_s": (c1["synapse_updates"] - c0["synapse_updates"]) / (d1 - d0),
+                                  "synapses": sim.synapses, "engine": sim.engine, "exact": sim.exact,
+                                  "sample_steps": steps}
+        sim.close()
+    except Exception as e:
+        out["brunel_plus_1e8"] = {"error": str(e)}
+    return out
+
+
 def main():
     args = parse()
     ensure_world(args)
@@ -456,6 +496,8 @@ def main():
     # the CPU reference sample runs after every GPU timed region (it builds a
     # 4.2 GB network and would share host memory bandwidth with the e2e leg)
     sim.close()
+    if rank == 0 and world == 1 and not args.no_secondary:
+        line["secondary"] = secondary_configs(synq)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu_result = {}
         try:
