@@ -247,17 +247,25 @@ SWEEP_S, SWEEP_STEPS = 1_000_000, 2000
 SWEEP = [(p, r) for p in (0.1, 0.01, 0.001) for r in (1.0, 10.0, 100.0)]
 
 
-def sweep_vectors():
+# the same model at S = 1e8 (N up to 316,228: the streamed-state ELL engine
+# of the sparse points), 100 Hz, 300 steps
+SWEEP_BIG_S, SWEEP_BIG_STEPS = 100_000_000, 300
+SWEEP_BIG = [(0.1, 100.0), (0.01, 100.0), (0.001, 100.0)]
+
+
+def sweep_vectors(S=None, steps=None, points=None, name="sweep.npz"):
     """Reference runs of the sweep model (include/synq/models/sweep.hpp built
     against the reference headers): per-step counts + digests, final ACC
     (sha256), counters."""
     import tempfile
+    S = S or SWEEP_S
+    steps = steps or SWEEP_STEPS
     out, meta = {}, {}
-    for p, rate in SWEEP:
+    for p, rate in (points or SWEEP):
         tag = f"sweep_p{p:g}_r{rate:g}"
         with tempfile.TemporaryDirectory() as td:
             base = os.path.join(td, "run")
-            O.golden("sweep", SWEEP_S, p, rate, 1, SWEEP_STEPS, base)
+            O.golden("sweep", S, p, rate, 1, steps, base)
             counts, ids = O.split_frames(np.fromfile(base + ".frames", np.uint32))
             acc = np.fromfile(base + ".state", np.uint32)
             counters = {}
@@ -266,22 +274,24 @@ def sweep_vectors():
                 counters[k] = int(v)
         out[f"{tag}_counts"] = counts
         out[f"{tag}_digests"] = frame_digests(counts, ids)
-        meta[tag] = {"S": SWEEP_S, "p": p, "rate": rate, "seed": 1, "steps": SWEEP_STEPS,
+        meta[tag] = {"S": S, "p": p, "rate": rate, "seed": 1, "steps": steps,
                      "acc_sha256": hashlib.sha256(acc.tobytes()).hexdigest(), "counters": counters}
-    np.savez_compressed(os.path.join(HERE, "sweep.npz"), **out)
+    np.savez_compressed(os.path.join(HERE, name), **out)
     return meta
 
 
 def main():
     if not O.have_reference():
         raise SystemExit("oracle/_ref not built (needs /root/reference): make -C oracle")
-    if sys.argv[1:] and sys.argv[1] in ("big", "sweep", "bigp"):
+    if sys.argv[1:] and sys.argv[1] in ("big", "sweep", "bigp", "sweepbig"):
         path = os.path.join(HERE, "golden.json")
         meta = json.load(open(path))
         if sys.argv[1] == "big":
             meta["big"] = big_vectors()
         elif sys.argv[1] == "bigp":
             meta["bigp"] = bigp_vectors()
+        elif sys.argv[1] == "sweepbig":
+            meta["sweep_big"] = sweep_vectors(SWEEP_BIG_S, SWEEP_BIG_STEPS, SWEEP_BIG, "sweep_big.npz")
         else:
             meta["sweep"] = sweep_vectors()
         with open(path, "w") as fh:

@@ -48,3 +48,26 @@ def test_sweep_points_bit_exact(golden, tmp_path):
         got = dict(line.strip().split("=") for line in open(base + ".counters"))
         for k in ("spikes", "deliveries", "frames_consumed", "edges", "neurons"):
             assert int(got[k]) == m["counters"][k], (tag, k)
+
+
+def test_sweep_points_at_1e8_bit_exact(golden, tmp_path):
+    """S = 1e8, 100 Hz, 300 steps (tests/golden/make_golden.py sweepbig):
+    N = 31,623 / 100,000 / 316,228 — the bitmap engine and the
+    streamed-state ELL engine of the sparse points at scale."""
+    if "sweep_big" not in golden["meta"]:
+        pytest.skip("sweep_big goldens not generated")
+    if not os.path.exists(BIN):
+        subprocess.run(["make", "-s", "-C", ROOT, "build/sweep"], check=True)
+    sw = np.load(os.path.join(ROOT, "tests", "golden", "sweep_big.npz"))
+    for tag, m in golden["meta"]["sweep_big"].items():
+        base = str(tmp_path / tag)
+        subprocess.run([BIN, "dump", str(m["S"]), repr(m["p"]), repr(m["rate"]), str(m["seed"]), str(m["steps"]),
+                        base], check=True, timeout=600)
+        counts, ids = O.split_frames(np.fromfile(base + ".frames", np.uint32))
+        assert np.array_equal(counts, sw[f"{tag}_counts"]), tag
+        assert np.array_equal(digests(counts, ids), sw[f"{tag}_digests"]), tag
+        acc = np.fromfile(base + ".state", np.uint32)
+        assert hashlib.sha256(acc.tobytes()).hexdigest() == m["acc_sha256"], tag
+        got = dict(line.strip().split("=") for line in open(base + ".counters"))
+        for k in ("spikes", "deliveries", "frames_consumed", "edges", "neurons"):
+            assert int(got[k]) == m["counters"][k], (tag, k)
