@@ -52,6 +52,18 @@ constexpr int kChunkBatch = 8;  // 16-byte row chunks in flight per lane during 
 enum prof_slot : int { P_UPDATE = 0, P_PUBLISH, P_POLL, P_GATHER, P_DELIVER, P_STEPS, P_SLOTS = 16 };
 // pipelined kernel only: 6 delivery wait for frames, 7 delivery passes,
 // 8 update first barrier, 9 update scan, 10 delivery frame prefixes,
+// NVLink peer exchange (engine_options::shard_peer): the step kernel stores
+// this shard's frames straight into every other shard's queue ring and its
+// publisher word there (peer-mapped memory), so a sharded run needs no host
+// exchange between launches
+struct peer_link {
+    uint32_t* queue;            // the peer's Q x n queue ring
+    unsigned long long* finfo;  // the peer's Q x E frame words
+    uint32_t E;                 // the peer's publisher count
+    uint32_t entry;             // this shard's publisher entry there
+};
+constexpr int kMaxPeers = 32;
+
 // 11 delivery chunk list
 
 template <class M>
@@ -103,6 +115,12 @@ struct persist_state {
     uint32_t stream_mode;  // bitmap delivery: barrier-free work items instead of passes
     uint32_t max_pass;     // frames per delivery pass (<= the polling warps)
     uint32_t dbg;          // timing experiments only (SYNQ_DBG): bit 1 = bitmap passes skip staging + counting
+    // peer exchange: every other shard's ring (npeers = 0: none); this
+    // shard's A / B id ranges start at a_lo / b_lo
+    const peer_link* peers;
+    uint32_t npeers;
+    uint32_t a_lo, b_lo;
+    volatile uint32_t* progress;  // SYNQ_WATCHDOG: 8 words per CTA, host-mapped
     // fold table (k_fold_table): tab[n0 * (T1 + 1) + n1] = fl-sum from +0 of
     // n0 copies of delta[0] then n1 copies of delta[1]; nullptr: no table
     const float* fold_tab;
@@ -126,6 +144,15 @@ SYNQ_DEV unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
     return v;
 }
 SYNQ_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+SYNQ_DEV unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+SYNQ_DEV void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+SYNQ_DEV void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 template <class M>
 SYNQ_DEV int source_class(const persist_state<M>& ps, uint32_t src) {
@@ -262,6 +289,10 @@ SYNQ_DEV bool frame_prefix(const persist_state<M>& ps, int64_t f, uint32_t* seg,
         }
     }
     if (nonblocking && !__all_sync(0xffffffffu, ok)) return false;
+    // peer entries were released by another GPU at system scope: acquire them
+    // at that scope (the words are complete, this re-read synchronises)
+    if (ps.npeers)
+        for (uint32_t j = ps.C + lane; j < E; j += 32) (void)ld_acquire_sys(fi + j);
     fence_acq_rel_gpu();  // acquire: the slices are visible to this CTA
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
@@ -643,22 +674,18 @@ template <class M>
 __global__ void k_log_drain(persist_state<M> ps, int64_t from, int64_t to) {
     __shared__ uint32_t s_seg[kMaxPieces + 1];
     __shared__ uint32_t s_lo[kMaxPieces + 1];
+    __shared__ uint32_t s_psrc[kMaxPieces];
+    __shared__ unsigned long long s_fval[kMaxTiles];
     const uint32_t P = ps.P;
     for (uint32_t j = threadIdx.x; j <= P; j += blockDim.x) s_lo[j] = ps.piece_lo[j];
+    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) s_psrc[j] = ps.piece_src[j];
     unsigned long long lc = 0;
     for (int64_t f = from; f <= to; ++f) {
         const uint32_t slot = static_cast<uint32_t>(f % ps.Q);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t run = 0;
-            for (uint32_t j = 0; j < P; ++j) {
-                s_seg[j] = run;
-                const uint32_t src = ps.piece_src[j];
-                const unsigned long long e = ps.finfo[static_cast<uint64_t>(slot) * ps.E + (src >> 1)];
-                run += word_half(e, src & 1);
-            }
-            s_seg[P] = run;
-        }
+        // every publisher's word of frame f (peer shards publish theirs
+        // asynchronously: wait for them), then the piece prefix
+        if (threadIdx.x < 32) frame_prefix(ps, f, s_seg, s_fval, s_psrc, false);
         __syncthreads();
         const uint32_t S = s_seg[P];
         if (threadIdx.x == 0) ps.log_cnt[f - from] = S;
@@ -823,6 +850,43 @@ __global__ void k_check_persist(persist_state<M> ps, int64_t t0, uint32_t b) {
 // id b_lo_r + i spiked (wa_max / wb_max = the largest A / B range of any
 // rank, in words).  Fixed size, so the allgather needs no counts exchange
 // and no host synchronisation.
+// Warp-wide: copy this shard's part of frame f (its local pieces, complete
+// and acquired by the caller) into every peer's ring as one consolidated
+// A slice and one B slice in ascending id order, then release the frame's
+// publisher word there (system scope: the stores cross NVLink).
+template <class M>
+SYNQ_DEV void peer_export(const persist_state<M>& ps, int64_t f) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t slot = static_cast<uint64_t>(f % ps.Q);
+    const unsigned long long* fi = ps.finfo + slot * ps.E;
+    const uint32_t* q = ps.queue + slot * ps.n;
+    uint32_t tot[2];
+    for (uint32_t half = 0; half < 2; ++half) {
+        const uint32_t dlo = half ? ps.b_lo : ps.a_lo;
+        uint32_t run = 0;
+        for (uint32_t c0 = 0; c0 < ps.C; c0 += 32) {
+            const uint32_t cc = c0 + lane;
+            const uint32_t cnt = cc < ps.C ? word_half(__ldcg(fi + cc), half) : 0u;
+            const uint32_t incl = warp_incl_scan(cnt);
+            const uint32_t src = cc < ps.C ? ps.piece_lo[ps.cta_piece[2 * cc + half]] : 0u;
+            const uint64_t dst = slot * ps.n + dlo + run + incl - cnt;
+            for (uint32_t j = 0; j < cnt; ++j) {
+                const uint32_t id = __ldcg(q + src + j);
+                for (uint32_t p = 0; p < ps.npeers; ++p) ps.peers[p].queue[dst + j] = id;
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        tot[half] = run;
+    }
+    __syncwarp();
+    fence_acq_rel_sys();  // every lane's slice stores before the words
+    __syncwarp();
+    for (uint32_t p = lane; p < ps.npeers; p += 32) {
+        const peer_link L = ps.peers[p];
+        st_relaxed_sys(L.finfo + slot * L.E + L.entry, frame_word(f, tot[0], tot[1]));
+    }
+}
+
 struct xbits_layout {
     uint32_t wa, wb;   // words per step of the A / B part (max over ranks)
     uint32_t steps;    // steps per block (delay - 1)

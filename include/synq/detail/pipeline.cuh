@@ -706,6 +706,17 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t pitch4 = ps.pitch >> 2;
         const uint32_t cap = ps.stage_items;
         uint32_t r_next = 1;
+        // peer exchange: this CTA exports the frames f = c (mod C) published
+        // by this launch, each as soon as its local pieces are complete
+        const int64_t last_pub = t0 + nrel - 1;
+        int64_t next_exp = t0 + static_cast<int64_t>((c + C - static_cast<uint32_t>(t0 % C)) % C);
+        auto try_export = [&]() {
+            while (next_exp <= last_pub && frame_complete(ps, next_exp, false, C)) {
+                fence_acq_rel_gpu();
+                peer_export(ps, next_exp);
+                next_exp += C;
+            }
+        };
         // frames before 0 do not exist: nothing to deliver (engine.hpp:371-380)
         if (fbase + 1 < 0) {
             const int64_t last_neg = -1 - fbase;  // rel of frame -1
@@ -719,7 +730,26 @@ __global__ void __launch_bounds__(NT, 1)
             if (dwarp < min(static_cast<uint32_t>(MB), ps.max_pass)) {
                 const uint32_t r = r_next + dwarp;
                 bool ok = false;
-                if (dwarp == 0) {
+                if (dwarp == 0 && ps.npeers) {
+                    // the same waits, spinning: the exports of this CTA's
+                    // frames may not wait behind the remote part of frame r
+                    for (;;) {
+                        if (ps.progress && lane == 0) {
+                            volatile uint32_t* w = ps.progress + 8 * c;
+                            w[0] = r;
+                            w[1] = static_cast<uint32_t>(next_exp - t0);
+                            w[2] = ld_acquire_cta(&s_updated);
+                            w[3] = ld_acquire_cta(&s_delivered);
+                            w[4] = 1;
+                        }
+                        try_export();
+                        if (r >= R && ld_acquire_cta(&s_updated) < r - R + 1) continue;
+                        if (ps.lag && !frame_complete(ps, fbase + r + ps.lag, false, ps.C)) continue;
+                        if (frame_prefix(ps, fbase + r, s_seg[0], s_fval[0], s_psrc, true)) break;
+                    }
+                    if (profiling) mark(6);
+                    ok = true;
+                } else if (dwarp == 0) {
                     // ring slot r % R is free once update step r - R folded it
                     if (r >= R) wait_at_least(&s_updated, r - R + 1);
                     if (ps.lag) frame_complete(ps, fbase + r + ps.lag, true, ps.C);  // local publishers only
@@ -993,6 +1023,17 @@ __global__ void __launch_bounds__(NT, 1)
             if (profiling) s_prof[7] += 1;
             r_next += B;
         }
+        if (dwarp == 0 && ps.npeers)  // the rest of this launch's frames (local completion only)
+            while (next_exp <= last_pub) {
+                if (ps.progress && lane == 0) {
+                    ps.progress[8 * c + 1] = static_cast<uint32_t>(next_exp - t0);
+                    ps.progress[8 * c + 4] = 2;
+                }
+                frame_complete(ps, next_exp, true, C);
+                fence_acq_rel_gpu();
+                peer_export(ps, next_exp);
+                next_exp += C;
+            }
         for (int o = 16; o; o >>= 1) my_deliv += __shfl_xor_sync(0xffffffffu, my_deliv, o);
         if (lane == 0 && my_deliv) atomicAdd(&ps.counters[C_DELIVERIES], my_deliv);
         if (log_cta && dtid == 0) {

@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -81,7 +82,23 @@ struct engine_options {
     // engine allgathers the spike frames itself after every batch
     bool shard_nccl = false;
     std::array<char, 128> nccl_id{};
+    // NVLink peer exchange: the step kernel stores this shard's frames
+    // straight into every other shard's queue ring (peer-mapped memory), so
+    // run() is one persistent launch per batch with no host exchange.
+    // Connect with connect_peers (same process) or connect_peers_ipc; with
+    // shard_nccl the engine exchanges the IPC handles over NCCL itself.
+    bool shard_peer = false;
 };
+
+// one shard's peer-exchange buffers (device pointers in the owner's space)
+struct peer_endpoint {
+    uint32_t* queue = nullptr;
+    unsigned long long* finfo = nullptr;
+    uint32_t publishers = 0;
+    uint32_t reserved = 0;
+};
+// cudaIpcMemHandle_t of the queue ring and of the frame words + publishers
+constexpr size_t kPeerHandleBytes = 2 * 64 + 8;
 
 struct engine_counters {
     uint64_t steps = 0;
@@ -206,6 +223,7 @@ public:
             if (stream_) cudaStreamSynchronize(stream_);
             detail::nccl_comm_destroy(nccl_);
         }
+        for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
         if (side_) {
             cudaStreamSynchronize(side_);
             cudaStreamDestroy(side_);
@@ -279,7 +297,11 @@ public:
 
     void run(int64_t steps) {
         if (steps <= 0) return;
-        if (sharded() && !nccl_) {
+        if (opt_.shard_peer && !peers_connected_) {
+            if (!nccl_) throw std::logic_error("peer shard: connect_peers / connect_peers_ipc before run");
+            if constexpr (population_model) exchange_ipc_handles();
+        }
+        if (sharded() && !nccl_ && !opt_.shard_peer) {
             // a shard may only run steps whose due frames are all present:
             // at most delay-1 steps past the frames imported from every rank
             if (steps > int64_t(delay_) - 1)
@@ -302,20 +324,20 @@ public:
             bool pending = false;
             // in-engine exchange: batches of at most delay-1 steps, each
             // followed by export -> ncclAllGather -> import on this stream
-            int64_t cap = nccl_ ? std::min<int64_t>(batch_cap_, int64_t(delay_) - 1) : int64_t(batch_cap_);
+            int64_t cap = nccl_xchg() ? std::min<int64_t>(batch_cap_, int64_t(delay_) - 1) : int64_t(batch_cap_);
             // debug_checks: the frames of a batch are checked after it, so a
             // batch may not outrun the queue ring (Q slots)
             if (opt_.debug_checks) cap = std::min<int64_t>(cap, Q_);
             while (steps > 0) {
                 const int64_t b = std::min<int64_t>(steps, cap);
                 if constexpr (population_model)
-                    if (nccl_) {
+                    if (nccl_xchg()) {
                         last_batch_t0_ = t_;
                         last_batch_b_ = static_cast<uint32_t>(b);
                     }
                 launch_persistent(static_cast<uint32_t>(b), slot);
                 if constexpr (population_model)
-                    if (nccl_) {
+                    if (nccl_xchg()) {
                         enqueue_export_bits(last_batch_t0_, last_batch_b_, xsend_.get());
                         detail::nccl_allgather_u32(nccl_, xsend_.get(), xrecv_.get(), xl_.block, stream_);
                         enqueue_import_bits(last_batch_t0_, last_batch_b_, xrecv_.get());
@@ -330,7 +352,7 @@ public:
             if (flags_host_[1]) throw device_error("ordered delivery scratch overflow");
             if (flags_host_[2]) throw device_error("sharded run: imported frames of a different batch length");
             check_debug_flags();
-            if (log_on_ && logged_upto_ < t_ && (!sharded() || nccl_)) drain_log();
+            if (log_on_ && logged_upto_ < t_ && (!sharded() || nccl_ || opt_.shard_peer)) drain_log();
         } else {
             while (steps > 0) {
                 const int64_t b = std::min<int64_t>(steps, batch_cap_);
@@ -416,7 +438,73 @@ public:
     // ---- multi-GPU shard exchange -------------------------
     // a shard of a multi-GPU run; an in-engine NCCL exchange is a shard even
     // with one rank (then the allgather copies the rank's own block)
-    bool sharded() const { return opt_.shard_world > 1 || opt_.shard_nccl; }
+    bool sharded() const { return opt_.shard_world > 1 || opt_.shard_nccl || opt_.shard_peer; }
+    const engine_options& options() const { return opt_; }
+    // frames exchanged by export -> ncclAllGather -> import after every batch
+    bool nccl_xchg() const { return nccl_ != nullptr && !opt_.shard_peer; }
+
+    // ---- NVLink peer exchange (engine_options::shard_peer) ---------------
+    // this shard's ring and frame words, for the other shards' kernels
+    peer_endpoint peer_buffers() const {
+        if (!opt_.shard_peer || !persistent_) throw std::logic_error("peer_buffers: not a peer shard");
+        return {queue_.get(), finfo_.get(), publishers_, 0};
+    }
+    // eps[q]: shard q's buffers as this process addresses them (eps[rank]
+    // is ignored).  Same-device shards of one process can pass the pointers
+    // of peer_buffers() directly; across processes use connect_peers_ipc.
+    void connect_peers(const std::vector<peer_endpoint>& eps) {
+        const uint32_t W = opt_.shard_world, R = opt_.shard_rank;
+        if (!opt_.shard_peer || !persistent_) throw std::logic_error("connect_peers: not a peer shard");
+        if (eps.size() != W) throw std::invalid_argument("connect_peers: need one endpoint per rank");
+        if (W - 1 > uint32_t(dev::kMaxPeers)) throw std::invalid_argument("connect_peers: too many ranks");
+        std::vector<dev::peer_link> links;
+        for (uint32_t q = 0; q < W; ++q) {
+            if (q == R) continue;
+            const peer_endpoint& e = eps[q];
+            if (!e.queue || !e.finfo || e.publishers < W) throw std::invalid_argument("connect_peers: bad endpoint");
+            const uint32_t Cq = e.publishers - (W - 1);  // the peer's local CTAs come first
+            links.push_back({e.queue, e.finfo, e.publishers, Cq + (R < q ? R : R - 1)});
+        }
+        peers_dev_.resize(std::max<size_t>(1, links.size()));
+        if (!links.empty()) peers_dev_.upload(links.data(), links.size(), stream_);
+        SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        npeers_ = static_cast<uint32_t>(links.size());
+        peers_connected_ = true;
+    }
+    // kPeerHandleBytes: IPC handles of this shard's ring and frame words
+    void peer_ipc_handle(void* out) const {
+        const peer_endpoint e = peer_buffers();
+        cudaIpcMemHandle_t hq{}, hf{};
+        SYNQ_CUDA(cudaIpcGetMemHandle(&hq, e.queue));
+        SYNQ_CUDA(cudaIpcGetMemHandle(&hf, e.finfo));
+        auto* b = static_cast<char*>(out);
+        std::memset(b, 0, kPeerHandleBytes);
+        std::memcpy(b, &hq, sizeof hq);
+        std::memcpy(b + 64, &hf, sizeof hf);
+        std::memcpy(b + 128, &e.publishers, 4);
+    }
+    // all: world x kPeerHandleBytes (rank q's handle at q * kPeerHandleBytes)
+    void connect_peers_ipc(const void* all) {
+        const uint32_t W = opt_.shard_world, R = opt_.shard_rank;
+        const auto* b = static_cast<const char*>(all);
+        std::vector<peer_endpoint> eps(W);
+        for (uint32_t q = 0; q < W; ++q) {
+            if (q == R) continue;
+            cudaIpcMemHandle_t hq{}, hf{};
+            std::memcpy(&hq, b + q * kPeerHandleBytes, sizeof hq);
+            std::memcpy(&hf, b + q * kPeerHandleBytes + 64, sizeof hf);
+            void *pq = nullptr, *pf = nullptr;
+            SYNQ_CUDA(cudaIpcOpenMemHandle(&pq, hq, cudaIpcMemLazyEnablePeerAccess));
+            ipc_opened_.push_back(pq);
+            SYNQ_CUDA(cudaIpcOpenMemHandle(&pf, hf, cudaIpcMemLazyEnablePeerAccess));
+            ipc_opened_.push_back(pf);
+            eps[q].queue = static_cast<uint32_t*>(pq);
+            eps[q].finfo = static_cast<unsigned long long*>(pf);
+            std::memcpy(&eps[q].publishers, b + q * kPeerHandleBytes + 128, 4);
+        }
+        connect_peers(eps);
+    }
+    bool peers_connected() const { return peers_connected_; }
     // words needed to export the frames of the last run() (upper bound)
     uint64_t export_capacity() const {
         return 1 + 2ull * (delay_ ? delay_ : 1) + uint64_t(delay_) * ((shard_lo_[1] - shard_lo_[0]) + (shard_lo_[3] - shard_lo_[2]));
@@ -880,8 +968,6 @@ private:
         uint32_t C = solo ? 1u : (clus ? CLn : (opt_.tiles ? opt_.tiles : tiles_for(n_)));
         C = std::min<uint32_t>({C, static_cast<uint32_t>(sms_), static_cast<uint32_t>(dev::kMaxTiles), n_});
         const uint32_t max_local = 4 * NTH;  // register-resident state: <= 4 neurons per thread
-        if (!solo && !clus && uint64_t(C) * max_local < n_)
-            C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (n_ + max_local - 1) / max_local));
         // shards: contiguous rank ranges of the receiving region (by receive
         // cost) and of the update-only region (by count); then this rank's
         // range into C local pieces of each kind
@@ -890,10 +976,11 @@ private:
         auto cut_cost = [&](uint32_t lo, uint32_t hi, uint32_t parts) { return cut_by_cost(prefix, r0, lo, hi, parts); };
         const std::vector<uint32_t> ra = W > 1 ? cut.ra : std::vector<uint32_t>{r0, r1};
         const std::vector<uint32_t> ub = W > 1 ? cut.ub : std::vector<uint32_t>{u0, u1};
-        if (W > 1) {  // the local shard sizes its CTA count by its own neurons
-            const uint64_t mine = (ra[R + 1] - ra[R]) + (ub[R + 1] - ub[R]);
-            if (!opt_.tiles) C = tiles_for(static_cast<int64_t>(mine));
-        }
+        // the local shard sizes its CTA count by its own neurons
+        const uint64_t mine = W > 1 ? uint64_t(ra[R + 1] - ra[R]) + (ub[R + 1] - ub[R]) : uint64_t(n_);
+        if (W > 1 && !opt_.tiles) C = tiles_for(static_cast<int64_t>(mine));
+        if (!solo && !clus && uint64_t(C) * max_local < mine)
+            C = static_cast<uint32_t>(std::min<uint64_t>(sms_, (mine + max_local - 1) / max_local));
         if (C + W - 1 > uint32_t(dev::kMaxTiles)) return;
         if (2ull * delay_ >= (1u << 15)) return;  // 16-bit frame tags need Q << 65536
         const std::vector<uint32_t> alo = cut_cost(ra[R], ra[R + 1], C), blo = cut_by_count(ub[R], ub[R + 1], C);
@@ -1054,6 +1141,13 @@ private:
     // k_import_bits); the NCCL communicator only with opt.shard_nccl
     void setup_exchange() requires population_model {
         const uint32_t W = opt_.shard_world, R = opt_.shard_rank;
+        if (opt_.shard_peer) {
+            // frames go straight into the peers' rings from the pipelined
+            // step kernel (pipeline.cuh peer_export)
+            if (!pipe_) throw std::invalid_argument("peer shard: needs the pipelined step kernel");
+            if (opt_.shard_nccl) nccl_ = detail::nccl_comm_init(R, W, opt_.nccl_id.data());
+            return;
+        }
         uint32_t wa = 1, wb = 1;
         for (uint32_t q = 0; q < W; ++q) {
             wa = std::max(wa, (all_ra_[q + 1] - all_ra_[q] + 31) / 32);
@@ -1076,6 +1170,20 @@ private:
             xrecv_.resize(size_t(W) * xl_.block);
             nccl_ = detail::nccl_comm_init(R, W, opt_.nccl_id.data());
         }
+    }
+
+    // shard_peer + shard_nccl: allgather the IPC handles over NCCL, map them
+    void exchange_ipc_handles() requires population_model {
+        const uint32_t W = opt_.shard_world;
+        constexpr size_t words = kPeerHandleBytes / 4;
+        pinned_array<uint32_t> h(words * W);
+        peer_ipc_handle(h.get());
+        dev_array<uint32_t> send(words), recv(words * W);
+        send.upload(h.get(), words, stream_);
+        detail::nccl_allgather_u32(nccl_, send.get(), recv.get(), words, stream_);
+        SYNQ_CUDA(cudaMemcpyAsync(h.get(), recv.get(), words * W * 4, cudaMemcpyDeviceToHost, stream_));
+        SYNQ_CUDA(cudaStreamSynchronize(stream_));
+        connect_peers_ipc(h.get());
     }
 
     // this shard's frames of steps [t0, t0+b) -> its bitmask block at `out`
@@ -1356,6 +1464,10 @@ private:
             cfg.attrs = at;
             cfg.numAttrs = 1;
             SYNQ_CUDA(cudaLaunchKernelExC(&cfg, kernel_fn(), args));
+        } else if (opt_.shard_peer) {
+            // one CTA per SM, co-resident by occupancy; a plain launch lets
+            // same-device shards of one process run side by side
+            SYNQ_CUDA(cudaLaunchKernel(kernel_fn(), dim3(tiles_), dim3(kernel_threads()), args, smem_, stream_));
         } else {
             SYNQ_CUDA(cudaLaunchCooperativeKernel(kernel_fn(), dim3(tiles_), dim3(kernel_threads()), args, smem_,
                                                   stream_));
@@ -1405,6 +1517,10 @@ private:
         p.E = publishers_;
         p.queue = queue_.get();
         p.finfo = finfo_.get();
+        p.peers = npeers_ ? peers_dev_.get() : nullptr;
+        p.npeers = npeers_;
+        p.a_lo = shard_lo_[0];
+        p.b_lo = shard_lo_[2];
         p.Q = Q_;
         p.K = K_;
         std::copy(bound_, bound_ + dev::kMaxClasses, p.bound);
@@ -1442,7 +1558,18 @@ private:
         if (const char* e = std::getenv("SYNQ_MAXPASS")) p.max_pass = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         p.stream_mode = 0;
         if (const char* e = std::getenv("SYNQ_WORKQ")) p.stream_mode = std::atoi(e) != 0 ? 1u : 0u;
+        if (opt_.shard_peer) p.stream_mode = 0;  // the exports run in the pass-mode poller
         p.dbg = 0;
+        p.progress = nullptr;
+        if (std::getenv("SYNQ_WATCHDOG")) {
+            if (!progress_.get()) {
+                progress_.resize(size_t(8) * tiles_);
+                std::memset(progress_.get(), 0, size_t(32) * tiles_);
+            }
+            uint32_t* d = nullptr;
+            SYNQ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), progress_.get(), 0));
+            p.progress = d;
+        }
         if (const char* e = std::getenv("SYNQ_DBG")) p.dbg = static_cast<uint32_t>(std::atoi(e));
         return p;
     }
@@ -1712,6 +1839,24 @@ private:
     // wait for slot `slot`'s batch and do its host bookkeeping / emission
     void finish_persistent(int slot) {
         batch_slot& fl = slots_[slot];
+        if (const char* e = std::getenv("SYNQ_WATCHDOG"); e && progress_.get()) {
+            // debugging aid: the delivery pollers' progress after a timeout
+            const auto t_end = clock::now() + std::chrono::duration<double>(std::atof(e));
+            while (cudaEventQuery(fl.ev[2]) == cudaErrorNotReady) {
+                if (clock::now() > t_end) {
+                    std::fprintf(stderr, "[synq watchdog] rank %u t0 %lld C %u\n", opt_.shard_rank,
+                                 static_cast<long long>(fl.t0), tiles_);
+                    for (uint32_t c = 0; c < tiles_; ++c) {
+                        const volatile uint32_t* w = progress_.get() + 8 * c;
+                        std::fprintf(stderr, "  cta %u: r_next %u next_exp-t0 %u updated %u delivered %u where %u\n", c,
+                                     w[0], w[1], w[2], w[3], w[4]);
+                    }
+                    std::fflush(stderr);
+                    std::abort();
+                }
+                std::this_thread::sleep_for(std::chrono::milliseconds(10));
+            }
+        }
         SYNQ_CUDA(cudaEventSynchronize(fl.ev[2]));
         float ms = 0;
         SYNQ_CUDA(cudaEventElapsedTime(&ms, fl.ev[0], fl.ev[1]));
@@ -1934,6 +2079,12 @@ private:
     dev::xbits_layout xl_{};
     dev_array<uint32_t> xremotes_, xsend_, xrecv_;
     void* nccl_ = nullptr;  // ncclComm_t of the in-engine exchange
+    // peer exchange: links to the other shards' rings, IPC mappings
+    dev_array<dev::peer_link> peers_dev_;
+    uint32_t npeers_ = 0;
+    bool peers_connected_ = false;
+    std::vector<void*> ipc_opened_;
+    pinned_array<uint32_t> progress_;  // SYNQ_WATCHDOG: per-CTA poller progress (mapped)
     std::array<uint32_t, 4> shard_lo_{};           // this shard: A [lo, hi), B [lo, hi)
     shard_cut cut_;                                // W > 1: rank ranges from the description
     std::vector<int64_t> imported_upto_;            // frames < this imported, per rank

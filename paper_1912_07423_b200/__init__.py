@@ -143,6 +143,11 @@ def lib() -> C.CDLL:
     sig("synq_sim_shard_bits_words", u64, vp)
     sig("synq_sim_shard_export_bits", st, vp, vp)
     sig("synq_sim_shard_import_bits", st, vp, vp)
+    sig("synq_opts_shard_peer", st, vp, C.c_int)
+    sig("synq_sim_peer_endpoint", st, vp, C.POINTER(PeerEndpoint))
+    sig("synq_sim_peer_connect", st, vp, C.POINTER(PeerEndpoint), u32)
+    sig("synq_sim_peer_ipc_handle", st, vp, vp)
+    sig("synq_sim_peer_connect_ipc", st, vp, vp, u32)
     _lib = L
     return L
 
@@ -162,7 +167,7 @@ class Opts:
     def __init__(self, seed=None, threads=None, deterministic=None, dt=None, delay=None,
                  record=None, defaults_file=None, params=None, batch_steps=None,
                  persistent=None, tiles=None, profile=None, shard=None, pipeline=None, lead=0,
-                 shard_nccl=None):
+                 shard_nccl=None, shard_peer=None):
         self._L = lib()  # kept: module globals may be gone when __del__ runs at exit
         self.h = self._L.synq_opts_new()
         if not self.h:
@@ -201,6 +206,8 @@ class Opts:
             rank, world, uid = shard_nccl
             buf = C.create_string_buffer(bytes(uid), 128)
             check(L.synq_opts_shard_nccl(self.h, int(rank), int(world), buf))
+        if shard_peer is not None:  # NVLink peer exchange (after shard / shard_nccl)
+            check(L.synq_opts_shard_peer(self.h, int(shard_peer)))
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -442,6 +449,27 @@ class Sim:
     def shard_import_bits(self, device_ptr: int):
         check(lib().synq_sim_shard_import_bits(self.h, C.c_void_p(device_ptr)))
 
+    # ---- NVLink peer exchange (Opts(shard_peer=True))
+    def peer_endpoint(self) -> "PeerEndpoint":
+        e = PeerEndpoint()
+        check(lib().synq_sim_peer_endpoint(self.h, C.byref(e)))
+        return e
+
+    def peer_connect(self, endpoints):
+        """endpoints[q]: every rank's peer_endpoint() (same process)."""
+        arr = (PeerEndpoint * len(endpoints))(*endpoints)
+        check(lib().synq_sim_peer_connect(self.h, arr, len(endpoints)))
+
+    def peer_ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+        check(lib().synq_sim_peer_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def peer_connect_ipc(self, handles):
+        """handles[q]: every rank's peer_ipc_handle() (other processes)."""
+        blob = b"".join(bytes(h) for h in handles)
+        check(lib().synq_sim_peer_connect_ipc(self.h, C.create_string_buffer(blob, len(blob)), len(handles)))
+
     def kernel_launches(self) -> int:
         return int(lib().synq_sim_kernel_launches(self.h))
 
@@ -449,6 +477,15 @@ class Sim:
         out = np.zeros(2, np.uint64)
         check(lib().synq_sim_transfer_bytes(self.h, _p(out)))
         return int(out[0]), int(out[1])
+
+
+PEER_HANDLE_BYTES = 136  # synq.h SYNQ_PEER_HANDLE_BYTES
+
+
+class PeerEndpoint(C.Structure):
+    """synq_peer_endpoint: a shard's queue ring and frame words."""
+    _fields_ = [("queue", C.c_void_p), ("finfo", C.c_void_p), ("publishers", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 def _prefer_torch_nccl():

@@ -85,6 +85,11 @@ public:
     virtual uint64_t shard_bits_words() const = 0;
     virtual void shard_export_bits(void* dst) = 0;
     virtual void shard_import_bits(const void* all) = 0;
+    virtual synq::peer_endpoint peer_endpoint() const = 0;
+    virtual void peer_connect(const std::vector<synq::peer_endpoint>& eps) = 0;
+    virtual void peer_ipc_handle(void* out) const = 0;
+    virtual void peer_connect_ipc(const void* all) = 0;
+    virtual uint32_t shard_world() const = 0;
 
     void write_stats(std::ostream& out) const;
     void write_stats_to(const std::string& path) const;
@@ -153,6 +158,11 @@ public:
     uint64_t shard_bits_words() const override { return net_->exchange_block_words(); }
     void shard_export_bits(void* dst) override { net_->export_bits(static_cast<uint32_t*>(dst)); }
     void shard_import_bits(const void* all) override { net_->import_bits(static_cast<const uint32_t*>(all)); }
+    synq::peer_endpoint peer_endpoint() const override { return net_->peer_buffers(); }
+    void peer_connect(const std::vector<synq::peer_endpoint>& eps) override { net_->connect_peers(eps); }
+    void peer_ipc_handle(void* out) const override { net_->peer_ipc_handle(out); }
+    void peer_connect_ipc(const void* all) override { net_->connect_peers_ipc(all); }
+    uint32_t shard_world() const override { return net_->options().shard_world; }
     void set_record(bool on) override {
         record_ = on;
         raster_.records.clear();  // keeps its capacity: a recurring recording reuses the pages
@@ -737,6 +747,52 @@ synq_status synq_opts_shard_nccl(synq_opts* o, uint32_t rank, uint32_t world, co
     o->cfg.engine.shard_nccl = true;
     std::memcpy(o->cfg.engine.nccl_id.data(), id, o->cfg.engine.nccl_id.size());
     return SYNQ_OK;
+}
+static_assert(SYNQ_PEER_HANDLE_BYTES == synq::kPeerHandleBytes, "peer handle size");
+static_assert(sizeof(synq_peer_endpoint) == sizeof(synq::peer_endpoint), "peer endpoint layout");
+synq_status synq_opts_shard_peer(synq_opts* o, int enable) {
+    SYNQ_CHECK_HANDLE(o);
+    o->cfg.engine.shard_peer = enable != 0;
+    return SYNQ_OK;
+}
+synq_status synq_sim_peer_endpoint(const synq_sim* s, synq_peer_endpoint* out) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(out);
+    return guarded([&] {
+        const synq::peer_endpoint e = s->impl->peer_endpoint();
+        *out = synq_peer_endpoint{e.queue, e.finfo, e.publishers, 0};
+        return SYNQ_OK;
+    });
+}
+synq_status synq_sim_peer_connect(synq_sim* s, const synq_peer_endpoint* eps, uint32_t world) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(eps);
+    return guarded([&] {
+        if (world != s->impl->shard_world()) throw std::invalid_argument("peer_connect: world differs from the shard's");
+        std::vector<synq::peer_endpoint> v(world);
+        for (uint32_t q = 0; q < world; ++q)
+            v[q] = {static_cast<uint32_t*>(eps[q].queue), static_cast<unsigned long long*>(eps[q].finfo),
+                    eps[q].publishers, 0};
+        s->impl->peer_connect(v);
+        return SYNQ_OK;
+    });
+}
+synq_status synq_sim_peer_ipc_handle(const synq_sim* s, void* out) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(out);
+    return guarded([&] {
+        s->impl->peer_ipc_handle(out);
+        return SYNQ_OK;
+    });
+}
+synq_status synq_sim_peer_connect_ipc(synq_sim* s, const void* all, uint32_t world) {
+    SYNQ_CHECK_HANDLE(s);
+    SYNQ_CHECK_HANDLE(all);
+    return guarded([&] {
+        if (world != s->impl->shard_world()) throw std::invalid_argument("peer_connect_ipc: world differs from the shard's");
+        s->impl->peer_connect_ipc(all);
+        return SYNQ_OK;
+    });
 }
 uint64_t synq_sim_shard_bits_words(const synq_sim* s) { return s ? s->impl->shard_bits_words() : 0; }
 synq_status synq_sim_shard_export_bits(synq_sim* s, void* dst) {

@@ -205,6 +205,62 @@ class ShardGroup:
             s.close()
 
 
+class PeerGroup:
+    """W peer-exchange shards of one network in one process (one GPU).
+
+    Opts(shard_peer=True): every shard's step kernel stores its frames into
+    the other shards' queue rings and releases them there
+    (include/synq/detail/persistent.cuh peer_export), so run(steps) is one
+    run() per shard with no exchange between launches.  The W kernels wait
+    on each other's frames and must run side by side: each shard gets
+    `tiles` CTAs (W x tiles <= the SM count), and the shards run from one
+    host thread each.  Across GPUs the same kernels run one per device,
+    connected through IPC handles (Sim.peer_ipc_handle / peer_connect_ipc).
+    """
+
+    def __init__(self, model: str, neurons: int, world: int, tiles: int = 8, synapses: int | None = None, **opts):
+        self.world = world
+        self.sims = [Sim(model, neurons, Opts(shard=(r, world), shard_peer=True, tiles=tiles, **opts),
+                         synapses=synapses) for r in range(world)]
+        self.delay = self.sims[0].delay
+        eps = [s.peer_endpoint() for s in self.sims]
+        for s in self.sims:
+            s.peer_connect(eps)
+
+    def run(self, steps: int):
+        import threading
+
+        errors: list[BaseException] = []
+
+        def go(s):
+            try:
+                s.run(steps)
+            except BaseException as e:  # re-raised below
+                errors.append(e)
+
+        threads = [threading.Thread(target=go, args=(s,)) for s in self.sims]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+
+    def neuron_field(self, f: int, dtype=np.float32) -> np.ndarray:
+        return assemble_field([(s.shard_range(), s.neuron_field(f, dtype)) for s in self.sims])
+
+    def counters(self) -> dict:
+        out: dict = {}
+        for s in self.sims:
+            for k, v in s.counters().items():
+                out[k] = out.get(k, 0) + v
+        return out
+
+    def close(self):
+        for s in self.sims:
+            s.close()
+
+
 class ShardedSim:
     """This process's shard of a network, exchanging frames over
     torch.distributed (launch one process per GPU with torchrun)."""

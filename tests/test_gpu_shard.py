@@ -229,3 +229,105 @@ def test_shard_stores_only_its_sub_rows(world):
     assert np.array_equal(np.array([len(f) for f in grp.frames]), counts)
     assert np.array_equal(np.concatenate(grp.frames), ids)
     grp.close()
+
+
+@pytest.mark.timeout(600, method="thread")
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_peer_exchange_bit_exact(golden, world):
+    """NVLink peer exchange (Opts(shard_peer=True)): the shards' step kernels
+    store their frames into each other's rings, run side by side on this GPU
+    (W x 8 CTAs), and every shard runs all steps in one run() call — no
+    exchange between launches.  Frames (each shard's engine log holds the
+    merged frames), state and counters equal the reference bit for bit."""
+    runs = golden["runs"]
+    n_cases = 0
+    for tag, m in population_runs(golden):
+        g = shard.PeerGroup(m["model"], m["neurons"], world, seed=m["seed"], deterministic=True, record=True,
+                            dt=m["dt"] or None, delay=m["delay"] or None)
+        assert all(s.persistent and s.pipelined for s in g.sims)
+        g.run(m["steps"])
+        for s in g.sims:
+            counts, ids = s.frames()
+            assert np.array_equal(counts, runs[f"{tag}_counts"]), (tag, world)
+            assert np.array_equal(ids, runs[f"{tag}_ids"]), (tag, world)
+        for i in range(3):
+            assert np.array_equal(g.neuron_field(i).view(np.uint32), runs[f"{tag}_f{i}"]), (tag, world, i)
+        c, rc = g.counters(), m["counters"]
+        assert c["spikes"] == rc["spikes"] and c["deliveries"] == rc["deliveries"], (tag, world)
+        g.close()
+        n_cases += 1
+    assert n_cases >= 2
+
+
+@pytest.mark.timeout(600, method="thread")
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_exchange_batches_and_brunel_scale(world):
+    """Peer shards across many launches (batch_steps 7 and 1000, runs cut
+    at odd sizes) and at a network whose frames carry hundreds of ids: the
+    merged raster equals the unsharded engine's."""
+    n = 20000
+    ref = synq.Sim("brunel", n, synq.Opts(seed=3, deterministic=True, record=True))
+    ref.run(1200)
+    rc, rids = ref.frames()
+    rv = ref.neuron_field(0).view(np.uint32).copy()
+    ref.close()
+    for batch in (7, 1000):
+        g = shard.PeerGroup("brunel", n, world, tiles=16, seed=3, deterministic=True, record=True, batch_steps=batch)
+        for k in (1, 250, 949):
+            g.run(k)
+        counts, ids = g.sims[1].frames()
+        assert np.array_equal(counts, rc), batch
+        assert np.array_equal(ids, rids), batch
+        assert np.array_equal(g.neuron_field(0).view(np.uint32), rv), batch
+        g.close()
+
+
+def _peer_worker(rank, world, port, m, out_dir):
+    """One peer shard per process: IPC handles swapped over gloo, then the
+    step kernels exchange frames through each other's memory."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sim = synq.Sim(m["model"], m["neurons"], synq.Opts(shard=(rank, world), shard_peer=True, tiles=4,
+                                                           record=True, seed=m["seed"], deterministic=True,
+                                                           dt=m["dt"] or None, delay=m["delay"] or None))
+        handles = [None] * world
+        dist.all_gather_object(handles, sim.peer_ipc_handle())
+        sim.peer_connect_ipc(handles)
+        dist.barrier()
+        sim.run(m["steps"])
+        counts, ids = sim.frames()
+        rng = sim.shard_range()
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=ids, counts=counts, rng=np.array(rng).reshape(-1),
+                 v=sim.neuron_field(0))
+        dist.barrier()  # the peer's ring stays mapped until both are done
+        sim.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_peer_exchange_ipc_processes(golden):
+    """Two processes on this GPU, one peer shard each, connected through
+    cudaIpc handles (the multi-GPU wiring; here the two contexts share the
+    device by time-slicing, so only a short run).  Each process's engine log
+    holds the merged frames of the reference."""
+    import torch.multiprocessing as mp
+
+    runs = golden["runs"]
+    tag, m = next(iter(population_runs(golden)))
+    m = dict(m, steps=min(m["steps"], 200))
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_peer_worker, args=(2, _free_port(), m, d), nprocs=2, join=True, start_method="spawn")
+        want_c = runs[f"{tag}_counts"][: m["steps"]]
+        want_ids = runs[f"{tag}_ids"][: int(want_c.sum())]
+        parts = []
+        for r in range(2):
+            z = np.load(os.path.join(d, f"r{r}.npz"))
+            assert np.array_equal(z["counts"], want_c), r
+            assert np.array_equal(z["ids"], want_ids), r
+            rg = z["rng"]
+            parts.append((((rg[0], rg[1]), (rg[2], rg[3])), z["v"]))
+        assert len(shard.assemble_field(parts)) == m["neurons"]
