@@ -66,6 +66,16 @@ constexpr bool model_trace_stdp() {
         return false;
 }
 
+// receive reads only the weight field W (== field 0) and writes no synapse
+// field (a trace_stdp trait declaration): stage W once, no write-back
+template <class M>
+constexpr bool model_receive_weight_only() {
+    if constexpr (requires { trace_stdp<M>::receive_reads_weight_only; })
+        return trace_stdp<M>::receive_reads_weight_only && trace_stdp<M>::W == 0;
+    else
+        return false;
+}
+
 // a model exposing plastic(src, dst) declares update_synapse a no-op for the
 // other synapses (benchmarks.hpp brunel_plus_model): catch-up skips them
 
@@ -933,6 +943,7 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
     using NF = typename M::neuron_fields;
     using SF = typename synapse_fields_of<M>::type;
     constexpr bool kSyn = synapse_fields_of<M>::present;
+    constexpr bool kWOnly = kSyn && model_receive_weight_only<M>();
     constexpr int NW = BLOCK / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_spk[kWinSpikes], s_sb[kWinSpikes], s_off[kWinSpikes + 1];
@@ -1041,9 +1052,13 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const uint32_t e = e0 + u * BLOCK + tid;
-                        if (e < E)
-                            stage_syn(st.sf, static_cast<uint64_t>(s_spk[ej[u]]) * st.deg_max + ek[u], s_syn, 2 * ecap,
-                                      e, ecap);
+                        if (e < E) {
+                            const uint64_t si = static_cast<uint64_t>(s_spk[ej[u]]) * st.deg_max + ek[u];
+                            if constexpr (kWOnly)
+                                reinterpret_cast<field_t<0, SF>*>(s_syn)[e] = st.sf.template get<0>()[si];
+                            else
+                                stage_syn(st.sf, si, s_syn, 2 * ecap, e, ecap);
+                        }
                     }
                 }
 #pragma unroll
@@ -1117,7 +1132,7 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
             }
             __syncthreads();
             // (6) synapse state written by receive (if any) goes back
-            if constexpr (kSyn) {
+            if constexpr (kSyn && !kWOnly) {
                 for (uint32_t e = tid; e < E; e += BLOCK) {
                     const uint32_t j = s_ev[e] >> 24, k = s_ev[e] & 0xffffffu;
                     unstage_syn(st.sf, static_cast<uint64_t>(s_spk[j]) * st.deg_max + k, s_syn, 2 * ecap, e, ecap);
