@@ -64,6 +64,10 @@ def parse():
                     help="skip the secondary BASELINE configs (Vogels 4000, Brunel+ 1e8) reported beside the headline")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent 1e9-synapse replicas instead of one sharded network")
+    ap.add_argument("--exchange", default="bitmask", choices=["bitmask", "peer"],
+                    help="N>1 with --backend nccl: bitmask = in-engine ncclAllGather of spike bitmasks every "
+                         "delay-1 steps; peer = NVLink peer exchange (the step kernel stores each frame into every "
+                         "peer's ring; IPC handles allgathered over NCCL; one launch per 1000 steps)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 frame exchange (gloo: host buffers, e.g. several ranks on one GPU)")
     return ap.parse_args()
@@ -543,8 +547,10 @@ def run_sharded(args, rank, world, local):
         # stream after every batch): one NCCL id, broadcast from rank 0
         uid = [synq.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
+        peer = args.exchange == "peer"
         sim = synq.Sim("brunel", opts=synq.Opts(seed=args.seed, deterministic=True,
-                                                shard_nccl=(rank, world, uid[0])), synapses=total)
+                                                shard_nccl=(rank, world, uid[0]), shard_peer=peer or None),
+                       synapses=total)
 
         class _Engine:  # the ShardedSim surface bench needs
             record = False
@@ -653,6 +659,8 @@ def run_sharded(args, rank, world, local):
                    "synapses": total_syn, "neurons": n, "synapses_per_gpu_max": max_syn,
                    "bio_s_per_step": 1.0, "dt_ms": 0.1, "delay_steps": sim.delay,
                    "parallelism": f"shard{world} (target-partitioned; " + (
+                       "NVLink peer exchange: the step kernel stores every frame into each peer's ring, "
+                       "system-scope release; IPC handles over NCCL)" if in_engine and args.exchange == "peer" else
                        f"in-engine ncclAllGather of spike bitmasks every {sim.delay - 1} steps)" if in_engine else
                        f"host-driven {args.backend} allgather of spike frames every {sim.delay - 1} steps)"),
                    "engine": f"{sim.engine} shard (exact)", "setup_s": round(setup_s, 2),

@@ -598,7 +598,45 @@ __global__ void k_catchup(M model, engine_state<M> st, int mode) {
 // k_catchup, bit for bit.
 SYNQ_DEV uint64_t rotr64(uint64_t x, uint32_t r) { return r ? (x >> r) | (x << (64 - r)) : x; }
 
+// pre bits of a replay window of n <= 64 steps from a0 (source history word
+// hw): bit j = the source spiked at a0 + j - delay (< 0: false)
+SYNQ_DEV uint64_t catchup_prew(uint64_t hw, int64_t a0, uint32_t delay, uint32_t n) {
+    const uint64_t lastn = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+    const int64_t p0 = a0 - static_cast<int64_t>(delay);
+    uint64_t prew = 0;
+    if (n <= 64 && p0 + static_cast<int64_t>(n) > 0) {
+        if (p0 >= 0) {
+            prew = rotr64(hw, static_cast<uint32_t>(p0 % 64));
+        } else {
+            const uint32_t neg = static_cast<uint32_t>(-p0);  // leading steps with u - delay < 0
+            prew = neg >= 64 ? 0ull : (hw << neg);             // bit j <- slot j - neg = u - delay
+        }
+    }
+    return prew & lastn;
+}
 
+// trace-STDP catch-up of one plastic synapse (rs -> rd) over the window from
+// a0: the traces are the neurons' P_src / Q_dst (trace_stdp), so only the
+// weight moves, at the window's events, with the decayed traces stdp_step
+// sees there (lif.hpp:78-89)
+template <class M>
+SYNQ_DEV float trace_catchup_weight(const engine_state<M>& st, const stdp_params& sp, uint32_t rs, uint32_t rd, int64_t a0,
+                                    uint64_t prew, uint64_t postu, float w) {
+    const uint64_t rn = st.n;  // step-major rings: [slot * n + neuron]
+    for (uint64_t ev = prew | postu; ev; ev &= ev - 1) {
+        const uint32_t e = static_cast<uint32_t>(__ffsll(static_cast<long long>(ev))) - 1;
+        const uint32_t um = static_cast<uint32_t>(a0 + e - 1) & (kTraceRing - 1);
+        if ((prew >> e) & 1ull) {
+            const float qt = st.tr_q[um * rn + rd] * sp.decay_minus;
+            w = clamp_weight(w - sp.a_minus * qt, sp.w_min, sp.w_max);
+        }
+        if ((postu >> e) & 1ull) {
+            const float pt = st.tr_p[um * rn + rs] * sp.decay_plus;
+            w = clamp_weight(w + sp.a_plus * pt, sp.w_min, sp.w_max);
+        }
+    }
+    return w;
+}
 
 // the catch-up list of step t: frame(due) U expiring (mode 0), or every
 // neuron (mode 1, flush through t - 1)
@@ -609,15 +647,16 @@ struct catchup_list {
     int64_t through = 0;
     // part 0: the whole list; 1: frame(due) only; 2: the expiring neurons
     // only, with t and their count from split_param (written by part 1: the
-    // expiring part may run beside the receive, whose epilogue advances t)
+    // expiring part may run beside the receive, whose epilogue advances t);
+    // 3: the expiring neurons only (frame(due) is caught up inside k_recv_win)
     int part = 0;
     SYNQ_DEV void load(const engine_state<M>& st, int mode, int64_t t, int part_ = 0) {
         part = part_;
         through = mode == 0 ? t : t - 1;
-        if (mode == 0 && part == 2) {
+        if (mode == 0 && (part == 2 || part == 3)) {
             frame = nullptr;
             ntr = 0;
-            total = static_cast<uint32_t>(st.split_param[1]);
+            total = part == 2 ? static_cast<uint32_t>(st.split_param[1]) : *st.expiring_count;
             return;
         }
         if (mode == 0) {
@@ -635,7 +674,7 @@ struct catchup_list {
     }
     SYNQ_DEV uint32_t at(const engine_state<M>& st, int mode, uint32_t k) const {
         if (mode == 1) return k;
-        if (part == 2) return st.expiring[k];
+        if (part >= 2) return st.expiring[k];
         return k < ntr ? frame[k] : st.expiring[k - ntr];
     }
 };
@@ -733,17 +772,7 @@ __global__ void __launch_bounds__(256, MINB) k_catchup1(M model, engine_state<M>
         if (k0 >= d) continue;
         const uint64_t lastn = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
         // pre bits: u - delay for u in [a0, through]; u - delay < 0 is false
-        const int64_t p0 = a0 - static_cast<int64_t>(st.delay);
-        uint64_t prew = 0;
-        if (n <= 64 && p0 + static_cast<int64_t>(n) > 0) {
-            if (p0 >= 0) {
-                prew = rotr64(hw, static_cast<uint32_t>(p0 % 64));
-            } else {
-                const uint32_t neg = static_cast<uint32_t>(-p0);  // leading steps with u - delay < 0
-                prew = neg >= 64 ? 0ull : (hw << neg);             // bit j <- slot j - neg = u - delay
-            }
-        }
-        prew &= lastn;
+        const uint64_t prew = catchup_prew(hw, a0, st.delay, n);
         const uint32_t r0 = static_cast<uint32_t>(a0 % 64);
         bool on[U];
         uint64_t postw[U];
@@ -766,26 +795,11 @@ __global__ void __launch_bounds__(256, MINB) k_catchup1(M model, engine_state<M>
                                          hist_bit(st, dst[u], x), st.dt);
             } else if (model_trace_stdp<M>() && st.tr_p) {
                 if constexpr (model_trace_stdp<M>()) {
-                    // the traces are the neurons' P_src / Q_dst (trace_stdp):
-                    // only the weight moves, at the window's events, with the
-                    // decayed traces stdp_step sees there (lif.hpp:78-89)
                     using T = trace_stdp<M>;
-                    const stdp_params& sp = T::params(model);
                     const uint64_t rs = nid, rd = dst[u], rn = st.n;  // step-major rings: [slot * n + neuron]
                     const uint64_t postu = rotr64(postw[u], r0) & lastn;
-                    float w = sv[u].template get<T::W>();
-                    for (uint64_t ev = prew | postu; ev; ev &= ev - 1) {
-                        const uint32_t e = static_cast<uint32_t>(__ffsll(static_cast<long long>(ev))) - 1;
-                        const uint32_t um = static_cast<uint32_t>(a0 + e - 1) & (kTraceRing - 1);
-                        if ((prew >> e) & 1ull) {
-                            const float qt = st.tr_q[um * rn + rd] * sp.decay_minus;
-                            w = clamp_weight(w - sp.a_minus * qt, sp.w_min, sp.w_max);
-                        }
-                        if ((postu >> e) & 1ull) {
-                            const float pt = st.tr_p[um * rn + rs] * sp.decay_plus;
-                            w = clamp_weight(w + sp.a_plus * pt, sp.w_min, sp.w_max);
-                        }
-                    }
+                    const float w = trace_catchup_weight(st, T::params(model), nid, dst[u], a0, prew, postu,
+                                                         sv[u].template get<T::W>());
                     const uint32_t ut = static_cast<uint32_t>(through) & (kTraceRing - 1);
                     sv[u].template get<T::W>() = w;
                     sv[u].template get<T::PT>() = st.tr_p[ut * rn + rs];
@@ -888,6 +902,9 @@ struct recv_win {
     uint32_t wmax;  // largest window (<= kWinTPT * block)
     uint32_t ecap;  // events staged per chunk
     uint32_t ages;  // advance the ages of the step's k_catchup1 list first
+    // trace-STDP models: catch up the due frame's rows inside the receive,
+    // window by window (k_catchup1 then takes the expiring neurons only)
+    uint32_t catchup;
 };
 constexpr int kWinTPT = 2;      // targets per thread (1024-thread CTAs)
 constexpr int kWinSpikes = 256;  // spikes per chunk (8 mask words per target)
@@ -938,15 +955,87 @@ SYNQ_DEV void unstage_syn(const field_ptrs<FieldList>& f, uint64_t i, const unsi
     }
 }
 
+// fused catch-up + weight staging for up to 4 events per thread (events
+// e = e_first + u * stride): the synapse of event e is caught up through t
+// exactly as k_catchup1 does (trace-STDP: weight moved at the window's events,
+// PT / QT = P_src(t) / Q_dst(t) stored; replay beyond 64 steps is not reached
+// under the expiry rule and replays step by step if it is), then its weight
+// is staged for the receive.  Loads of the four events go out together.
+template <class M>
+SYNQ_DEV void fused_catchup_stage(const M& model, const engine_state<M>& st, const uint32_t* s_spk, const uint32_t* s_cu_n,
+                                  const uint32_t* s_cu_a0, const unsigned long long* s_cu_prew, const float* s_cu_pt,
+                                  const uint32_t (&ej)[4], const uint32_t (&ek)[4], const uint32_t (&tg)[4],
+                                  uint32_t e_first, uint32_t stride, uint32_t E, int64_t t, uint32_t ut, float* s_w) {
+    if constexpr (model_trace_stdp<M>()) {
+        using T = trace_stdp<M>;
+        using SF = typename synapse_fields_of<M>::type;
+        float w[4], qn[4];
+        uint64_t post[4];
+        bool on[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t e = e_first + u * stride;
+            on[u] = false;
+            if (e < E) {
+                const uint32_t j = ej[u], src = s_spk[j];
+                const uint64_t si = static_cast<uint64_t>(src) * st.deg_max + ek[u];
+                w[u] = st.sf.template get<T::W>()[si];
+                on[u] = s_cu_n[j] != 0;
+                if constexpr (model_has_plastic<M>()) on[u] = on[u] && model.plastic(src, tg[u]);
+                if (on[u]) {
+                    post[u] = st.hist[tg[u]];
+                    qn[u] = st.tr_q[static_cast<uint64_t>(ut) * st.n + tg[u]];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t e = e_first + u * stride;
+            if (e >= E) continue;
+            if (on[u]) {
+                if constexpr (model_has_plastic<M>()) __builtin_assume(model.plastic(s_spk[ej[u]], tg[u]));
+                const uint32_t j = ej[u], src = s_spk[j], n = s_cu_n[j];
+                const int64_t a0 = s_cu_a0[j];
+                const uint64_t si = static_cast<uint64_t>(src) * st.deg_max + ek[u];
+                if (n <= 64) {
+                    const uint64_t lastn = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+                    const uint64_t postu = rotr64(post[u], static_cast<uint32_t>(a0 % 64)) & lastn;
+                    w[u] = trace_catchup_weight(st, T::params(model), src, tg[u], a0, s_cu_prew[j], postu, w[u]);
+                    st.sf.template get<T::W>()[si] = w[u];
+                    st.sf.template get<T::PT>()[si] = s_cu_pt[j];
+                    st.sf.template get<T::QT>()[si] = qn[u];
+                } else {
+                    synapse_state<SF> sv;
+                    load_syn(st.sf, si, sv);
+                    sv.src_ = src;
+                    sv.dst_ = tg[u];
+                    for (int64_t x = a0; x <= t; ++x)
+                        model.update_synapse(sv, hist_bit(st, src, x - static_cast<int64_t>(st.delay)),
+                                             hist_bit(st, tg[u], x), st.dt);
+                    store_syn(st.sf, si, sv);
+                    w[u] = sv.template get<T::W>();
+                }
+            }
+            s_w[e] = w[u];
+        }
+    }
+}
+
 template <class M, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st, recv_win rw) {
     using NF = typename M::neuron_fields;
     using SF = typename synapse_fields_of<M>::type;
     constexpr bool kSyn = synapse_fields_of<M>::present;
     constexpr bool kWOnly = kSyn && model_receive_weight_only<M>();
+    constexpr bool kFuse = kWOnly && model_trace_stdp<M>();
     constexpr int NW = BLOCK / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_spk[kWinSpikes], s_sb[kWinSpikes], s_off[kWinSpikes + 1];
+    // fused catch-up: per spike of the chunk, its replay window (steps, start, pre bits) and P_src(t)
+    constexpr int kCu = kFuse ? kWinSpikes : 1;
+    __shared__ uint32_t s_cu_n[kCu], s_cu_a0[kCu];
+    __shared__ unsigned long long s_cu_prew[kCu];
+    __shared__ float s_cu_pt[kCu];
     __shared__ uint32_t s_tmp[NW + 1];
     __shared__ uint32_t s_take;
     const uint32_t wmax = rw.wmax, ecap = rw.ecap;
@@ -966,6 +1055,26 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
 
     const uint32_t lo = rw.lo[c], wn = rw.lo[c + 1] - lo;
     unsigned long long mine = 0;
+    const bool fuse = kFuse && rw.catchup != 0;
+    const uint32_t ut = static_cast<uint32_t>(t) & (kTraceRing - 1);
+    if constexpr (kFuse) {
+        if (fuse && due >= 0) {
+            // the due frame's rows are caught up through t below, each window
+            // by its CTA; their synapse-update counters and caught flags once
+            // per row here (k_catchup1 semantics, engine.hpp:414-436)
+            const uint32_t S = st.qcount[due % st.Q];
+            const uint32_t* spikes = st.queue + static_cast<uint64_t>(due % st.Q) * st.n;
+            for (uint32_t k = c * BLOCK + tid; k < S; k += C * BLOCK) {
+                const uint32_t sid = spikes[k];
+                const int64_t a0 = st.ages[sid];
+                if (a0 <= t) {
+                    atomicAdd(&st.counters[C_SYN_UPDATES],
+                              static_cast<unsigned long long>(st.degree[sid]) * static_cast<unsigned long long>(t - a0 + 1));
+                    st.caught[sid] = 1;
+                }
+            }
+        }
+    }
     if (due >= 0 && wn > 0) {
         const uint32_t S = st.qcount[due % st.Q];
         const uint32_t* spikes = st.queue + static_cast<uint64_t>(due % st.Q) * st.n;
@@ -990,6 +1099,17 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
                 cnt = sp[1] - sb;
                 s_spk[tid] = sid;
                 s_sb[tid] = sb;
+                if constexpr (kFuse) {
+                    if (fuse) {  // the row's replay window [a0, t] (k_catchup1)
+                        const int64_t a0 = st.ages[sid];
+                        const bool on = (!st.row_plastic || st.row_plastic[sid]) && a0 <= t;
+                        const uint32_t n = on ? static_cast<uint32_t>(t - a0 + 1) : 0u;
+                        s_cu_n[tid] = n;
+                        s_cu_a0[tid] = static_cast<uint32_t>(a0);
+                        s_cu_prew[tid] = on ? catchup_prew(st.hist[sid], a0, st.delay, n) : 0ull;
+                        s_cu_pt[tid] = st.tr_p[static_cast<uint64_t>(ut) * st.n + sid];
+                    }
+                }
             }
             uint32_t incl = cnt;
 #pragma unroll
@@ -1048,16 +1168,26 @@ __global__ void __launch_bounds__(BLOCK) k_recv_win(M model, engine_state<M> st,
                 // output: with programmatic dependent launch this kernel got
                 // here while k_catchup1 was still running
                 if constexpr (kSyn) {
-                    if (g0 == 0 && e0 == 0) grid_dependency_wait();
+                    // (fused: the frame's rows are this kernel's own: no wait)
+                    if (g0 == 0 && e0 == 0 && !fuse) grid_dependency_wait();
+                    if constexpr (kFuse) {
+                        if (fuse) {
+                            fused_catchup_stage<M>(model, st, s_spk, s_cu_n, s_cu_a0, s_cu_prew, s_cu_pt, ej, ek, tg,
+                                                   e0 + tid, BLOCK, E, t, ut,
+                                                   reinterpret_cast<field_t<0, SF>*>(s_syn));
+                        }
+                    }
+                    if (!fuse) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const uint32_t e = e0 + u * BLOCK + tid;
-                        if (e < E) {
-                            const uint64_t si = static_cast<uint64_t>(s_spk[ej[u]]) * st.deg_max + ek[u];
-                            if constexpr (kWOnly)
-                                reinterpret_cast<field_t<0, SF>*>(s_syn)[e] = st.sf.template get<0>()[si];
-                            else
-                                stage_syn(st.sf, si, s_syn, 2 * ecap, e, ecap);
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t e = e0 + u * BLOCK + tid;
+                            if (e < E) {
+                                const uint64_t si = static_cast<uint64_t>(s_spk[ej[u]]) * st.deg_max + ek[u];
+                                if constexpr (kWOnly)
+                                    reinterpret_cast<field_t<0, SF>*>(s_syn)[e] = st.sf.template get<0>()[si];
+                                else
+                                    stage_syn(st.sf, si, s_syn, 2 * ecap, e, ecap);
+                            }
                         }
                     }
                 }

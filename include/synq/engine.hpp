@@ -1488,7 +1488,8 @@ private:
             return npt_ == 1 ? reinterpret_cast<const void*>(dev::k_solo<Model, 1>)
                              : (npt_ == 2 ? reinterpret_cast<const void*>(dev::k_solo<Model, 2>)
                                           : reinterpret_cast<const void*>(dev::k_solo<Model, 4>));
-        if (pipe_) return pipe_bm_ ? pipeline_fn<true>(pipe_uw_, pipe_npt_) : pipeline_fn<false>(pipe_uw_, pipe_npt_);
+        if (pipe_)
+            return pipe_bm_ ? pipeline_fn<true>(pipe_uw_, pipe_npt_) : pipeline_fn<false>(pipe_uw_, pipe_npt_);
         return persistent_fn();
     }
 
@@ -1600,6 +1601,24 @@ private:
         SYNQ_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
     }
 
+    // trace-STDP models on the windowed receive: k_recv_win catches up the
+    // due frame's rows itself (window by window, right before receiving them)
+    // and k_catchup1 takes the expiring neurons only.  Opt-in
+    // (SYNQ_FUSED_CATCHUP=1): bit-exact, but at Brunel+ 1e8 30.7-36.7 us per
+    // step against 29.6 for the separate catch-up (the expiring neurons'
+    // catch-up, not the frame's, is most of the catch-up time, and the
+    // receive's whole-SM CTAs then wait beside it).
+    bool fused_recv_catchup() const {
+        if constexpr (has_synapses && dev::model_trace_stdp<Model>() && dev::model_receive_weight_only<Model>()) {
+            const char* e = std::getenv("SYNQ_FUSED_CATCHUP");
+            if (!e || std::atoi(e) == 0) return false;
+            return win_on_ && (exact_ || !atomic_recv_) && static_cast<bool>(tr_p_) && hist_words_ == 1 &&
+                   !split_catchup_ && !pdl_all_;
+        } else {
+            return false;
+        }
+    }
+
     void enqueue_catchup(int mode, bool fuse_compact = false) {
         if constexpr (has_synapses) {
             if (hist_words_ == 1) {
@@ -1607,8 +1626,9 @@ private:
                 uint32_t g = static_cast<uint32_t>(sms_) * 4;
                 // mode 0 with a side stream: frame(due) here (the receive
                 // needs its synapses), the expiring neurons on side_ beside
-                // the receive (disjoint rows: expiring = not transmitting)
-                const int part = (mode == 0 && split_catchup_) ? 1 : 0;
+                // the receive (disjoint rows: expiring = not transmitting);
+                // fused: the expiring neurons only (part 3)
+                const int part = (mode == 0 && split_catchup_) ? 1 : (mode == 0 && fused_recv_catchup()) ? 3 : 0;
                 // SYNQ_CATCHUP_U=2: 2 synapses per lane, 6 CTAs per SM (A/B)
                 const bool u2 = catchup_u_ == 2;
                 if (u2) g = static_cast<uint32_t>(sms_) * 6;
@@ -1682,7 +1702,9 @@ private:
             cfg.attrs = at;
             cfg.numAttrs = pdl ? 1 : 0;
             Model m = model_;
-            SYNQ_CUDA(cudaLaunchKernelEx(&cfg, dev::k_recv_win<Model, kWinBlock>, m, st, win_));
+            dev::recv_win rw = win_;
+            rw.catchup = fused_recv_catchup() ? 1u : 0u;
+            SYNQ_CUDA(cudaLaunchKernelEx(&cfg, dev::k_recv_win<Model, kWinBlock>, m, st, rw));
         } else if (exact_) {
             dev::k_det_events<Model, kReceiveBlock, false><<<rgrid, kReceiveBlock, 0, stream_>>>(st);
             dev::k_det_scan<Model, 1024><<<1, 1024, 0, stream_>>>(st);
@@ -1854,7 +1876,7 @@ private:
                     std::fflush(stderr);
                     std::abort();
                 }
-                std::this_thread::sleep_for(std::chrono::milliseconds(10));
+                std::this_thread::sleep_for(std::chrono::microseconds(50));
             }
         }
         SYNQ_CUDA(cudaEventSynchronize(fl.ev[2]));
