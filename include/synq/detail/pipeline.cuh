@@ -806,39 +806,61 @@ __global__ void __launch_bounds__(NT, 1)
                 const uint4* bmw = ps.bm + static_cast<uint64_t>(c) * WQ;
                 for (uint32_t g0 = 0; g0 < S; g0 += cap) {
                     const uint32_t n = min(cap, S - g0);
-                    // (1) spike ids: one per thread and pass position (its
-                    // frame by the pass prefix, its piece by binary search
-                    // over the frame's piece prefix); every thread issues
-                    // its 4-byte global->shared copies (cp.async), one wait
-                    for (uint32_t i = dtid; i < n; i += DT) {
-                        const uint32_t g = g0 + i;
-                        uint32_t w = 0;
+                    // (1)+(2) per warp and 32 pass positions: lane L loads the
+                    // spike id of position i0 + L (its frame by the pass
+                    // prefix, its piece by binary search over the frame's
+                    // piece prefix; L2 loads, the slices were acquired with
+                    // the frame words), records its (frame, class) group, and
+                    // the warp then issues the spikes' windows (16-byte
+                    // cp.async.cg, 32 / WQ spikes x WQ columns per
+                    // instruction, ids by shuffle) right away: no wait or
+                    // barrier between the id and the window of a spike
+                    const uint32_t spi = 32u >> wq_sh;  // spikes per window instruction
+                    const bool stage = (ps.dbg & 2) == 0;
+                    constexpr int kIdU = 4;  // id loads in flight per lane before their windows
+                    for (uint32_t b0 = dwarp * 32; b0 < n; b0 += DW * 32 * kIdU) {
+                        uint32_t srcv[kIdU];
 #pragma unroll
-                        for (int q = 1; q < MB; ++q)
-                            if (static_cast<uint32_t>(q) < B && fpre[q] <= g) w = q;
-                        const uint32_t gl = g - fpre[w];
-                        const uint32_t* seg = s_seg[w];
-                        const uint32_t a = piece_of(seg, P, gl);
-                        cp_async4(s_src + i, ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
-                        s_grp[i] = static_cast<uint8_t>(w);
-                    }
-                    cp_async_wait_all();
-                    named_bar(BAR_D, DT);
-                    // (frame, class) group of each spike; CTA 0 logs the frames
-                    for (uint32_t i = dtid; i < n; i += DT) {
-                        const uint32_t src = s_src[i], w = s_grp[i];
-                        if (w >= wlog && lbase + g0 + i < ps.log_cap) ps.log[lbase + g0 + i] = src;
-                        s_grp[i] = static_cast<uint8_t>(w * 4 + static_cast<uint32_t>(source_class(ps, src)));
+                        for (int k = 0; k < kIdU; ++k) {
+                            const uint32_t i = b0 + k * DW * 32 + lane;
+                            srcv[k] = 0;
+                            if (i < n) {
+                                const uint32_t g = g0 + i;
+                                uint32_t w = 0;
+#pragma unroll
+                                for (int q = 1; q < MB; ++q)
+                                    if (static_cast<uint32_t>(q) < B && fpre[q] <= g) w = q;
+                                const uint32_t gl = g - fpre[w];
+                                const uint32_t* seg = s_seg[w];
+                                const uint32_t a = piece_of(seg, P, gl);
+                                srcv[k] = __ldcg(ps.queue + s_qbase[w] + s_lo[a] + (gl - seg[a]));
+                                s_grp[i] = static_cast<uint8_t>(w);
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < kIdU; ++k) {
+                            const uint32_t i0 = b0 + k * DW * 32, i = i0 + lane;
+                            if (i0 >= n) break;
+                            const uint32_t src = srcv[k];
+                            if (i < n) {
+                                const uint32_t w = s_grp[i];
+                                s_src[i] = src;
+                                if (w >= wlog && lbase + g0 + i < ps.log_cap) ps.log[lbase + g0 + i] = src;
+                                s_grp[i] = static_cast<uint8_t>(w * 4 + static_cast<uint32_t>(source_class(ps, src)));
+                            }
+                            if (stage) {
+                                for (uint32_t j = 0; j < WQ; ++j) {
+                                    const uint32_t sl = j * spi + (lane >> wq_sh), q = lane & (WQ - 1);
+                                    const uint32_t sid = __shfl_sync(0xffffffffu, src, sl);
+                                    const uint32_t gg = i0 + sl;
+                                    if (gg < n)
+                                        cp_async16_cg(sw + gg * WQ + (q ^ ((gg >> swz_sh) & swz_m)),
+                                                      bmw + static_cast<uint64_t>(sid) * ps.bm_row4 + q);
+                                }
+                            }
+                        }
                     }
                     if (profiling) mark(P_GATHER);
-                    // (2) windows -> shared memory: 16-byte cp.async.cg copies,
-                    // all issued back to back, one wait
-                    const uint32_t items = (ps.dbg & 2) ? 0u : n * WQ;
-                    for (uint32_t it = dtid; it < items; it += DT) {
-                        const uint32_t g = it >> wq_sh, q = it & (WQ - 1);
-                        cp_async16_cg(sw + g * WQ + (q ^ ((g >> swz_sh) & swz_m)),
-                                      bmw + static_cast<uint64_t>(s_src[g]) * ps.bm_row4 + q);
-                    }
                     cp_async_wait_all();
                     named_bar(BAR_D, DT);
                     if (profiling) mark(11);

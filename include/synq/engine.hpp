@@ -1552,10 +1552,13 @@ private:
         p.bm_row4 = bm_row4_;
         p.wq = bm_wq_;
         p.bm_prefetch = pipe_bm_ && lag_ > 0 ? 1u : 0u;
-        p.max_pass = pipe_bm_ ? 6 : 8;  // bitmap: 6 frames per pass measured best at B1e9 (4.48 vs 4.66 us/step at 8)
-        // sharded launches hold delay-1 steps, all their frames complete at launch:
-        // 4 frames per pass (one-rank NCCL shard 91.0 vs 93.4 ms per bio-s at 6)
-        if (pipe_bm_ && sharded()) p.max_pass = 4;
+        // bitmap: 7 frames per pass measured best at B1e9 with the fused
+        // id / window staging (43.30 ms per bio-s; 6: 43.84, 8: 43.4, 4: 47.1)
+        p.max_pass = pipe_bm_ ? 7 : 8;
+        // NCCL-exchanging shards' launches hold delay-1 steps, all their frames
+        // complete at launch: 4 frames per pass (one-rank NCCL shard 91.0 vs
+        // 93.4 ms per bio-s at 6); peer shards run full-length launches
+        if (pipe_bm_ && sharded() && !opt_.shard_peer) p.max_pass = 4;
         if (const char* e = std::getenv("SYNQ_MAXPASS")) p.max_pass = static_cast<uint32_t>(std::max(1, std::atoi(e)));
         p.stream_mode = 0;
         if (const char* e = std::getenv("SYNQ_WORKQ")) p.stream_mode = std::atoi(e) != 0 ? 1u : 0u;
