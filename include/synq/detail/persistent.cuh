@@ -689,11 +689,12 @@ __global__ void k_log_drain(persist_state<M> ps, int64_t from, int64_t to) {
         __syncthreads();
         const uint32_t S = s_seg[P];
         if (threadIdx.x == 0) ps.log_cnt[f - from] = S;
-        for (uint32_t j = 0; j < P; ++j) {
-            const uint32_t cnt = s_seg[j + 1] - s_seg[j];
-            for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x)
-                if (lc + s_seg[j] + k < ps.log_cap)
-                    ps.log[lc + s_seg[j] + k] = ps.queue[static_cast<uint64_t>(slot) * ps.n + s_lo[j] + k];
+        // one thread per frame position (its piece by binary search over the
+        // piece prefix): every load and host store of the frame in flight at once
+        for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) {
+            const uint32_t a = piece_of(s_seg, P, i);
+            if (lc + i < ps.log_cap)
+                ps.log[lc + i] = ps.queue[static_cast<uint64_t>(slot) * ps.n + s_lo[a] + (i - s_seg[a])];
         }
         lc += S;
     }

@@ -27,6 +27,23 @@
 namespace synq {
 namespace {
 
+// f(a, b) over [0, n) split into contiguous ranges on up to 8 host threads
+// (large rasters); f must not throw
+template <class F>
+void parallel_ranges(size_t n, F&& f) {
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    if (n < (size_t(1) << 18) || hw == 1) {
+        f(size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t per = (n + hw - 1) / hw;
+    for (unsigned k = 1; k < hw; ++k)
+        pool.emplace_back([&f, n, per, k] { f(std::min(n, k * per), std::min(n, (k + 1) * per)); });
+    f(size_t(0), std::min(n, per));
+    for (auto& th : pool) th.join();
+}
+
 struct sim_config {  // sim_runtime.hpp:15-21
     param_set params = builtin_defaults();
     engine_options engine;
@@ -59,7 +76,9 @@ public:
     virtual uint64_t measured_spike_count() const = 0;
     virtual uint32_t measured_neurons() const = 0;
     virtual int64_t warmup_steps() const = 0;
-    virtual const spike_raster& raster() const = 0;
+    virtual const spike_raster& raster() const = 0;  // materialised on demand (file output)
+    virtual uint64_t raster_size() const = 0;
+    virtual void raster_copy(int64_t* steps, uint32_t* ids) const = 0;
     virtual bool persistent() const = 0;
     virtual bool pipelined() const = 0;
     virtual bool solo() const = 0;
@@ -165,13 +184,21 @@ public:
     uint32_t shard_world() const override { return net_->options().shard_world; }
     void set_record(bool on) override {
         record_ = on;
-        raster_.records.clear();  // keeps its capacity: a recurring recording reuses the pages
+        // the recorded raster is kept compact: the ids of every frame in
+        // order plus one (step, end) run per step with spikes; clear() keeps
+        // the capacity, so a recurring recording reuses the pages
+        rids_.clear();
+        rruns_.clear();
+        raster_.records.clear();
+        raster_valid_ = true;
         if (on)
             net_->set_spike_tap([this](int64_t t, std::span<const uint32_t> frame) {
-                auto& r = raster_.records;
-                const size_t o = r.size(), n = frame.size();
-                if (r.capacity() < o + n) r.reserve(std::max<size_t>(2 * r.capacity(), o + n + (size_t(1) << 20)));
-                for (size_t k = 0; k < n; ++k) r.push_back({t, frame[k]});
+                const size_t o = rids_.size(), n = frame.size();
+                if (n == 0) return;
+                if (rids_.capacity() < o + n) rids_.reserve(std::max<size_t>(2 * rids_.capacity(), o + n + (size_t(1) << 20)));
+                rids_.insert(rids_.end(), frame.begin(), frame.end());
+                rruns_.push_back({t, o + n});
+                raster_valid_ = false;
             });
         else
             net_->set_spike_tap(nullptr);
@@ -209,7 +236,30 @@ public:
     }
     uint32_t measured_neurons() const override { return me_ - mb_; }
     int64_t warmup_steps() const override { return warmup_; }
-    const spike_raster& raster() const override { return raster_; }
+    const spike_raster& raster() const override {
+        if (!raster_valid_) {
+            raster_.records.resize(rids_.size());
+            raster_copy_records(raster_.records.data());
+            raster_valid_ = true;
+        }
+        return raster_;
+    }
+    uint64_t raster_size() const override { return rids_.size(); }
+    // (steps, ids) of the recorded raster, split over host threads by record
+    // range (each range: its first run by binary search, then fills + copies)
+    void raster_copy(int64_t* steps, uint32_t* ids) const override {
+        parallel_ranges(rids_.size(), [&](size_t a, size_t b) {
+            size_t r = std::upper_bound(rruns_.begin(), rruns_.end(), a,
+                                        [](size_t x, const std::pair<int64_t, size_t>& run) { return x < run.second; }) -
+                       rruns_.begin();
+            for (size_t i = a; i < b; ++r) {
+                const size_t e = std::min(b, rruns_[r].second);
+                std::fill(steps + i, steps + e, rruns_[r].first);
+                std::memcpy(ids + i, rids_.data() + i, (e - i) * sizeof(uint32_t));
+                i = e;
+            }
+        });
+    }
     bool persistent() const override { return net_->persistent(); }
     bool pipelined() const override { return net_->pipelined(); }
     bool solo() const override { return net_->solo(); }
@@ -254,7 +304,21 @@ private:
     bool record_;
     int64_t warmup_ = 0;
     std::unique_ptr<network<M>> net_;
-    spike_raster raster_;
+    std::vector<uint32_t> rids_;                       // recorded ids, frame after frame
+    std::vector<std::pair<int64_t, size_t>> rruns_;  // (step, end in rids_) per step with spikes
+    mutable spike_raster raster_;                      // record form, built for file output
+    mutable bool raster_valid_ = true;
+    void raster_copy_records(spike_record* out) const {
+        parallel_ranges(rids_.size(), [&](size_t a, size_t b) {
+            size_t r = std::upper_bound(rruns_.begin(), rruns_.end(), a,
+                                        [](size_t x, const std::pair<int64_t, size_t>& run) { return x < run.second; }) -
+                       rruns_.begin();
+            for (size_t i = a; i < b; ++r) {
+                const size_t e = std::min(b, rruns_[r].second);
+                for (; i < e; ++i) out[i] = {rruns_[r].first, rids_[i]};
+            }
+        });
+    }
 };
 
 // sim_runtime.cpp:98-141 (+ engine line)
@@ -859,34 +923,17 @@ synq_status synq_sim_counters(const synq_sim* s, uint64_t out[6]) {
 synq_status synq_sim_raster_size(const synq_sim* s, uint64_t* out) {
     SYNQ_CHECK_HANDLE(s);
     SYNQ_CHECK_HANDLE(out);
-    *out = s->impl->raster().records.size();
+    *out = s->impl->raster_size();
     return SYNQ_OK;
 }
 synq_status synq_sim_raster_copy(const synq_sim* s, int64_t* steps, uint32_t* ids, uint64_t capacity) {
     SYNQ_CHECK_HANDLE(s);
-    const auto& r = s->impl->raster().records;
-    if (capacity < r.size() || (!r.empty() && (!steps || !ids))) {
+    const uint64_t n = s->impl->raster_size();
+    if (capacity < n || (n && (!steps || !ids))) {
         set_error("raster buffers too small or null");
         return SYNQ_ERR_INVALID_ARGUMENT;
     }
-    // large rasters are split into (steps, ids) by several host threads
-    auto part = [&](size_t a, size_t b) {
-        for (size_t i = a; i < b; ++i) {
-            steps[i] = r[i].step;
-            ids[i] = r[i].neuron;
-        }
-    };
-    const size_t n = r.size();
-    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-    if (n < (size_t(1) << 18) || hw == 1) {
-        part(0, n);
-    } else {
-        std::vector<std::thread> pool;
-        const size_t per = (n + hw - 1) / hw;
-        for (unsigned k = 1; k < hw; ++k) pool.emplace_back(part, std::min(n, k * per), std::min(n, (k + 1) * per));
-        part(0, std::min(n, per));
-        for (auto& th : pool) th.join();
-    }
+    s->impl->raster_copy(steps, ids);
     return SYNQ_OK;
 }
 synq_status synq_sim_step_spikes(const synq_sim* s, uint32_t* out, uint64_t capacity) {
