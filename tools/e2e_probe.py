@@ -19,7 +19,10 @@ for rec in (False, True, True, True):
     t2 = time.perf_counter()
     n = 0
     if rec:
-        st, ids = sim.raster()
+        if not hasattr(sim, "_bufs"):
+            import numpy as np
+            sim._bufs = (np.zeros(6_000_000, np.int64), np.zeros(6_000_000, np.uint32))
+        st, ids = sim.raster(out=sim._bufs)
         n = len(ids)
     t3 = time.perf_counter()
     print(f"record={rec}: run wall {1e3*(t1-t0):.1f} ms, device {1e3*(d1-d0):.1f} ms, kernel {1e3*(k1-k0):.1f} ms, "
