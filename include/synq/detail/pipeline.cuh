@@ -266,13 +266,28 @@ __global__ void __launch_bounds__(NT, 1)
             mark(P_POLL);
             uint32_t* cslot = ring + (s % R) * ps.K * ps.win_cap;
             uint32_t mcount = 0;
+            // chunk m + 1's state (and RNG) is loaded before chunk m is
+            // updated and stored (distinct neurons), so the loads of the next
+            // chunk are in flight while this one computes
+            values_t<NF> vn{};
+            xorshift rn;
+            auto fetch = [&](uint32_t m) {
+                const uint32_t j = tid + m * UT;
+                if (j < L) {
+                    const uint32_t i = id_of(j);
+                    load_all(ps.nf, i, vn);
+                    if constexpr (model_uses_rng<M>()) rn = ps.rng[i];
+                }
+            };
+            if (MC) fetch(0);
             for (uint32_t m = 0; m < MC; ++m) {
                 const uint32_t j = tid + m * UT;
                 bool sp = false;
+                values_t<NF> vl = vn;
+                xorshift rl = rn;
+                if (m + 1 < MC) fetch(m + 1);
                 if (j < L) {
                     const uint32_t i = id_of(j);
-                    values_t<NF> vl;
-                    load_all(ps.nf, i, vl);
                     if (j < na) {  // receiving neuron: fold frame rel s in class order
                         uint32_t a[kMaxClasses];
 #pragma unroll
@@ -282,13 +297,17 @@ __global__ void __launch_bounds__(NT, 1)
                         }
                         detail::pack_get<ACC>::get(vl) = fold_frame(ps, detail::pack_get<ACC>::get(vl), a);
                     }
-                    xorshift rl;
-                    bool ll = false;
+                    const xorshift r0 = rl;
+                    bool ll = model_uses_rng<M>();  // prefetched: rng() must not reload it
                     local_neuron<NF> ref{i, &vl, &rl, &ll, ps.rng};
                     sp = model.update(ref, ps.dt);
                     store_all(ps.nf, i, vl);
-                    if constexpr (model_uses_rng<M>())
-                        if (ll) ps.rng[i] = rl;
+                    if constexpr (model_uses_rng<M>()) {
+                        uint4 a, b;
+                        memcpy(&a, &rl, 16);
+                        memcpy(&b, &r0, 16);
+                        if (a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w) ps.rng[i] = rl;  // drawn from
+                    }
                     if (sp && i >= ps.meas_lo && i < ps.meas_hi) ++mcount;
                 }
                 const int na_here = static_cast<int>(na) - static_cast<int>(m * UT + warp * 32);
