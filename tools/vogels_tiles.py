@@ -9,7 +9,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1912_07423_b200 as synq
 
-for tiles in [int(x) for x in sys.argv[1:]] or [None, 8, 16, 24, 32, 48, 64]:
+for tiles in [int(x) or None for x in sys.argv[1:]] or [None, 8, 16, 24, 32, 48, 64]:
     sim = synq.Sim("vogels", 4000, synq.Opts(seed=1, deterministic=True, tiles=tiles))
     sim.run(2000)
     _, k0 = sim.device_time()
