@@ -120,3 +120,31 @@ def test_brunel_plus_at_scale_bit_exact(golden, tag):
     assert c["spikes"] == rc["spikes"] and c["deliveries"] == rc["deliveries"]
     assert c["synapse_updates"] == rc["synapse_updates"]
     sim.close()
+
+
+@pytest.mark.timeout(900, method="thread")
+def test_brunel_1e9_peer_shards_full_second_bit_exact(golden):
+    """The bench network as two NVLink-peer shards (Opts(shard_peer=True)),
+    side by side on this GPU with 74 CTAs each, one run() of the whole
+    biological second: each shard stores only its targets' sub-rows, the
+    step kernels store their frames into each other's rings, and every
+    shard's engine log (the merged frames) and the assembled state equal the
+    reference's, step for step."""
+    from paper_1912_07423_b200 import shard
+
+    m = golden["meta"]["big"][TAG]
+    big = golden["big"]
+    g = shard.PeerGroup(m["model"], 0, 2, tiles=74, synapses=m["synapses"], seed=m["seed"], deterministic=True,
+                        record=True)
+    assert sum(s.synapses for s in g.sims) == m["edges"]
+    g.run(m["steps"])
+    for r, s in enumerate(g.sims):
+        counts, ids = s.frames()
+        diff = np.nonzero(counts != big[f"{TAG}_counts"])[0]
+        assert len(diff) == 0, f"shard {r}: spike counts first differ at step {diff[0]}"
+        diff = np.nonzero(digests(counts, ids) != big[f"{TAG}_digests"])[0]
+        assert len(diff) == 0, f"shard {r}: spike ids first differ at step {diff[0]}"
+    for i in range(3):
+        f = g.neuron_field(i).view(np.uint32)
+        assert hashlib.sha256(f.tobytes()).hexdigest() == m["state_sha256"][i], i
+    g.close()
