@@ -27,11 +27,11 @@
 namespace synq {
 namespace {
 
-// f(a, b) over [0, n) split into contiguous ranges on up to 8 host threads
+// f(a, b) over [0, n) split into contiguous ranges on up to 16 host threads
 // (large rasters); f must not throw
 template <class F>
 void parallel_ranges(size_t n, F&& f) {
-    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     if (n < (size_t(1) << 18) || hw == 1) {
         f(size_t(0), n);
         return;
